@@ -1,0 +1,315 @@
+"""Benchmark: masked tokens/s scored (logprob + GRPO loss) on B200, % of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One *step* = one pass of the trainer-side hot path over one shard of the
+synthetic batch of BASELINE.json configs[1] (Qwen3-4B-shaped: 64 tasks x group
+8, 8K-token multi-turn trajectories, V = 151936, bf16 logits; only informative
+groups are scored, as IterationStats::informative hands over):
+H2D of the host SoA -> K1 pack -> K3 GRPO -> K2+K4 fused over every logits
+micro-batch -> NCCL all-reduce of the partials -> D2H, all through the C-ABI
+call prorl_score_host with pinned HOST buffers (the e2e number). `value` is
+the same step with its inputs resident in HBM: the device segments
+pack+GRPO+score+all-reduce timed with CUDA events on the launching stream.
+
+The logits are the LM-head stand-in (the model forward is out of the
+reference's scope): a pool of 3 micro-batch buffers (15 GB,
+>> the 126 MB L2) filled by the synthetic generator during warm-up; micro-batch
+j reads buffer j % 3, so no L2 reuse between micro-batches. Generation is not
+inside the timed region.
+
+Multi-GPU (torchrun): groups are sharded by deterministic LPT (no data-path
+collective); the only collective is the NCCL all-reduce of the 330-double
+partials inside each step. Timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG_NAMES = {"c1": 0, "c2": 1, "c3": 2, "c4": 3}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--microbatch", type=int, default=16576)  # 148 SMs x 8 warps x 14 rows
+    ap.add_argument("--pool", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def bytes_per_row(vocab: int, dtype: str) -> int:
+    # V * sizeof(logit) + ~26 B of side arrays per active row
+    # (target 4 + old_lp 4 + seq 4 + turn 2 + adv 4 + row bookkeeping 8)
+    return vocab * (2 if dtype == "bf16" else 4) + 26
+
+
+def measured_peak_gbs():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(shard, cfg, seed: int, budget_s: float) -> dict:
+    """The CPU oracle (a restatement of the path: the reference has no CPU
+    implementation of the math) timed on this host's cores over a bounded
+    sample of the same workload's active rows."""
+    from oracle import oracle as O
+    b = shard.batch
+    threads = os.cpu_count() or 1
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)
+    oc = O.score_cfg(cfg.vocab, cfg.dtype, microbatch_rows=cfg.microbatch_rows)
+    # calibrate on a small sample, then size the timed sample for ~budget_s
+    probe = O.score_batch(hb, oc, seed, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
+    rate = (threads * 4) / max(probe["timings"][1], 1e-6)
+    n = int(min(max(rate * budget_s, threads), shard.n_active))
+    r = O.score_batch(hb, oc, seed, 2.0, nthreads=threads, row_begin=0, row_end=n)
+    t_pack = r["timings"][0] * n / max(shard.n_active, 1)  # pack + GRPO amortised over the sample
+    value = n / (r["timings"][1] + t_pack)
+    return {"value": value, "unit": "masked tokens/s", "cores": threads, "kind": "port",
+            "sample": f"first {n} of {shard.n_active} active rows of the same shard (scoring time; logits "
+                      f"generation excluded; pack+GRPO of the full shard amortised pro rata)",
+            "seconds": float(r["timings"][1])}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path for this workload on the host
+    cores (the oracle port — the reference has no implementation of the math,
+    SPEC.md:8,741), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2603_18815_b200 import synth
+    shard = synth.make_shard(args.config)
+    c = synth.CONFIGS[args.config]
+    b = shard.batch
+    threads = os.cpu_count() or 1
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)
+    oc = O.score_cfg(c["vocab"], c["dtype"], microbatch_rows=args.microbatch)
+    probe = O.score_batch(hb, oc, 2603, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
+    rate = threads * 4 / max(probe["timings"][1], 1e-6)
+    per_step = int(min(max(rate * 6.0, threads), shard.n_active))  # ~6 s of CPU work per step
+    times = []
+    for s in range(args.warmup + args.steps):
+        r = O.score_batch(hb, oc, 2603, 2.0, nthreads=threads, row_begin=0, row_end=per_step)
+        t = r["timings"][1] + r["timings"][0] * per_step / max(shard.n_active, 1)
+        if s >= args.warmup:
+            times.append(t)
+    value = per_step * len(times) / sum(times)
+    line = {"metric": "masked tokens/sec scored (logprob+GRPO loss)", "value": value, "unit": "masked tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic", "impl": "reference",
+            "config": {"workload": c["desc"], "config_id": args.config, "active_rows_per_step": per_step,
+                       "parallelism": "cpu threads"},
+            "cpu_baseline": {"value": value, "unit": "masked tokens/s", "cores": threads, "kind": "port",
+                             "sample": f"first {per_step} active rows per step of the {args.config} shard"},
+            "e2e": {"value": value, "unit": "masked tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_18815_b200 import _native as N
+    from paper_2603_18815_b200 import synth
+    from paper_2603_18815_b200.hotpath import ScoreConfig, Scorer, finalize, nccl_unique_id
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = synth.CONFIGS[args.config]
+    shard = synth.make_shard(args.config, rank=rank, world=world)
+    host = shard.batch.pinned()
+    cfg = ScoreConfig(vocab=c["vocab"], dtype=c["dtype"], microbatch_rows=args.microbatch)
+    sc = Scorer(local)
+    if world > 1:
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sc.nccl_init(world, rank, uid[0])
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    pool = [torch.empty((args.microbatch, c["vocab"]), dtype=tdt, device="cuda") for _ in range(args.pool)]
+    stream = torch.cuda.current_stream()
+    n_mb = (shard.n_active + args.microbatch - 1) // args.microbatch
+
+    # warm-up: the first call fills the pool with generated logits (LM-head stand-in)
+    for w in range(max(args.warmup, 1)):
+        partials, tm = sc.score_host(host, cfg, pool, fill=(w == 0), seed=2603)
+    torch.cuda.synchronize()
+
+    # totals over ranks (weak scaling: each rank scores its own groups)
+    n_local = torch.tensor([shard.n_active], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(n_local)
+    n_total = int(n_local.item())
+
+    clocks = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    seg = np.zeros(5)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        partials, tm = sc.score_host(host, cfg, pool, fill=False, seed=2603)
+        seg += tm
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    e2e_ms = ev0.elapsed_time(ev1)
+    dev_ms = float(seg[1] + seg[2] + seg[3])  # pack+GRPO, score, all-reduce (inputs resident)
+    score_ms = float(seg[2])
+    t = torch.tensor([e2e_ms, dev_ms, score_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms, dev_ms, score_ms = (float(x) for x in t.tolist())
+    K = args.steps
+    value = n_total * K / (dev_ms / 1e3)
+    e2e = n_total * K / (e2e_ms / 1e3)
+
+    # roofline of the dominant kernel (fused K2+K4), from the live events
+    bpr = bytes_per_row(c["vocab"], c["dtype"])
+    local_rows = shard.n_active
+    peak, peak_kind = measured_peak_gbs()
+    achieved = local_rows * bpr * K / (seg[2] / 1e3) / 1e9  # rank-local bytes / rank-local score time
+    traffic = None
+    tf = ROOT / "profiles" / "k_score_traffic.json"
+    if tf.exists():
+        try:
+            tj = json.loads(tf.read_text())
+            traffic = tj["dram_bytes_per_row"] * min(args.microbatch, local_rows)
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        res = finalize(partials)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(shard, cfg, 2603, args.cpu_seconds)
+            except Exception as ex:  # the baseline must not sink the GPU number
+                cpu = {"error": repr(ex)}
+        launches_per_step = 6 + 3 + 1 + n_mb + 1  # 2 scans x3, seq_bounds/pack/compact, grpo, score x n_mb, reduce
+        line = {
+            "metric": "masked tokens/sec scored (logprob+GRPO loss)",
+            "value": value, "unit": "masked tokens/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": c["dtype"], "data": "synthetic",
+            "config": {"workload": c["desc"], "config_id": args.config, "parallelism": f"group-sharded dp{world}",
+                       "global_batch": f"{len(shard.groups)} informative groups on rank0, {n_total} active rows",
+                       "seq_len": c["tokens"], "vocab": c["vocab"], "microbatch_rows": args.microbatch,
+                       "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
+                       f"({args.pool * args.microbatch * c['vocab'] * (2 if c['dtype'] == 'bf16' else 4) / 1e9:.1f} GB)",
+                       "l2": "inputs larger than L2 (logits pool >> 126 MB; no flush needed)"},
+            "e2e": {"value": e2e, "unit": "masked tokens/s", "h2d_bytes_per_step": host.bytes_h2d(),
+                    "d2h_bytes_per_step": N.N_PARTIALS * 8, "ms_per_step": e2e_ms / K},
+            "gpu_launches": launches_per_step * K,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
+                         "kernel": "k_score<bf16,8,5,4096,fused> (K2+K4)", "bytes_per_row": bpr},
+            "segments_ms_per_step": {"h2d": seg[0] / K, "pack_grpo": seg[1] / K, "score": seg[2] / K,
+                                     "allreduce": seg[3] / K, "d2h": seg[4] / K},
+            "clocks": clk,
+            "result": {"loss": res["loss"], "entropy": res["entropy"], "clip_lo_frac": res["clip_lo_frac"],
+                       "clip_hi_frac": res["clip_hi_frac"], "n_active": res["n_active"]},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    sc.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,233 @@
+/*
+ * prorl_hotpath.h — C-ABI of the B200 (sm_100a) trainer-side scoring path for
+ * ProRL Agent (arXiv 2603.18815): pack -> logprob/entropy -> GRPO advantage ->
+ * DAPO clipped surrogate + per-turn metrics -> NCCL all-reduce of partials.
+ *
+ * The reference has no operator/FFI surface for this math; the
+ * drop-in surface it does own is the C++ trainer API.  Each entry point below
+ * names the reference interface it replaces or extends:
+ *
+ *   prorl_pack            extends  TokenTrajectory::flatten/flatten_range
+ *                                  (proj/include/rollout/trajectory.hpp:76-87,
+ *                                  role->mask rule at :82-83) and the id/logprob
+ *                                  fields of Turn (trajectory.hpp:27-33, types.hpp:12)
+ *   prorl_grpo_adv        extends  PromptGroup::usable_rewards + is_informative
+ *                                  (proj/src/trainer/harness.cpp:84-102)
+ *   prorl_logprob_entropy new      (absent in reference: SPEC.md:8)
+ *   prorl_clipped_loss    new      (absent in reference: SPEC.md:741; DAPO PAPER.md:368)
+ *   prorl_allreduce       new      (the reference has no collectives)
+ *   prorl_score_host      replaces the trajectory drop at
+ *                                  proj/src/trainer/harness.cpp:263-273 — the
+ *                                  whole per-GPU step from host SoA buffers.
+ *
+ * Conventions:
+ *   - every function returns 0 (PRORL_OK) or a negative prorl_status; the
+ *     message is in prorl_last_error() (thread-local);
+ *   - negative codes map 1:1 onto rollout::Error codes (errors.hpp:10-59) plus
+ *     three new ones (cuda_error, nccl_error, shape_mismatch);
+ *   - buffers are caller-owned device memory unless a name says host_; the
+ *     library only owns the workspace inside a ctx;
+ *   - all device work is stream-ordered on the stream argument, no implicit
+ *     device synchronisation (prorl_score_host and prorl_check_errors are the
+ *     documented exceptions: they synchronise their stream);
+ *   - one ctx per device; calls on distinct ctxs are thread-safe.
+ */
+#ifndef PRORL_HOTPATH_H
+#define PRORL_HOTPATH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRORL_ABI_VERSION 1
+
+typedef enum prorl_status {
+  PRORL_OK = 0,
+  PRORL_E_MALFORMED_TURN = -1,    /* rollout::MalformedTurn   "malformed_turn"   */
+  PRORL_E_INCOMPLETE_GROUP = -2,  /* rollout::IncompleteGroup "incomplete_group" */
+  PRORL_E_MALFORMED_REQUEST = -3, /* rollout::MalformedRequest "malformed_request" */
+  PRORL_E_CUDA = -10,             /* new: "cuda_error"      */
+  PRORL_E_NCCL = -11,             /* new: "nccl_error"      */
+  PRORL_E_SHAPE = -12,            /* new: "shape_mismatch"  */
+  PRORL_E_TOKEN_RANGE = -13,      /* new: "shape_mismatch" (token id outside [0,V)) */
+} prorl_status;
+
+typedef enum prorl_dtype { PRORL_BF16 = 0, PRORL_FP32 = 1 } prorl_dtype;
+
+/* rollout::Role order (trajectory.hpp:11). */
+enum { PRORL_ROLE_SYSTEM = 0, PRORL_ROLE_USER = 1, PRORL_ROLE_ASSISTANT = 2, PRORL_ROLE_TOOL = 3 };
+
+/* Number of per-turn metric buckets and the partials layout. */
+#define PRORL_TURN_BUCKETS 64
+#define PRORL_N_GLOBAL 10
+#define PRORL_N_PER_TURN 5
+#define PRORL_N_PARTIALS (PRORL_N_GLOBAL + PRORL_TURN_BUCKETS * PRORL_N_PER_TURN) /* 330 */
+enum {
+  PRORL_P_LOSS_SUM = 0, PRORL_P_N_ACTIVE = 1, PRORL_P_ENTROPY_SUM = 2, PRORL_P_LOGP_SUM = 3,
+  PRORL_P_RATIO_SUM = 4, PRORL_P_CLIP_LO = 5, PRORL_P_CLIP_HI = 6, PRORL_P_KL1_SUM = 7,
+  PRORL_P_ADV_SUM = 8, PRORL_P_N_ROLLOUTS = 9
+};
+/* per-turn bucket k starts at PRORL_N_GLOBAL + 5*k: [N_k, loss_k, H_k, logp_k, clip_k] */
+
+typedef struct prorl_ctx prorl_ctx;
+
+/* One turn descriptor. Turns are listed in trajectory order, trajectories in
+ * ascending `traj` (the rollout index inside the shard, = seq id). `src_off`
+ * indexes the flat wire arrays (ids, logprobs) passed alongside. */
+typedef struct prorl_turn_desc {
+  int64_t src_off;
+  int32_t traj;
+  int32_t len;
+  uint8_t role; /* PRORL_ROLE_* */
+  uint8_t pad_[7];
+} prorl_turn_desc;
+
+/* Packed outputs (device pointers, caller-owned). Sizes: N = total tokens,
+ * n_seq = number of trajectories (rollout slots), A = active rows. */
+typedef struct prorl_packed {
+  int32_t* tokens;     /* [N]   int32 token ids (range-checked < V)           */
+  uint8_t* loss_mask;  /* [N]   1 iff the token came from an ASSISTANT turn    */
+  int16_t* turn_id;    /* [N]   assistant-turn ordinal, -1 for others          */
+  int32_t* seq_id;     /* [N]   trajectory (rollout) index                     */
+  int32_t* pos_id;     /* [N]   position inside the sequence                   */
+  int32_t* cu_seqlens; /* [n_seq+1] exclusive prefix of sequence lengths        */
+  float* old_lp;       /* [N]   behaviour logprob (fp64 -> fp32 RN), 0 if mask=0 */
+  int32_t* act_row;    /* [A]   active rows r (token r+1 is a policy token)     */
+  int32_t* act_target; /* [A]   tokens[r+1]                                     */
+  float* act_old_lp;   /* [A]   old_lp[r+1]                                     */
+  int32_t* act_seq;    /* [A]   seq_id[r+1]                                     */
+  int16_t* act_turn;   /* [A]   turn_id[r+1]                                    */
+  int64_t* n_active;   /* [1]   device scalar                                   */
+} prorl_packed;
+
+typedef struct prorl_loss_cfg {
+  float eps_lo;       /* DAPO clip low  (default 0.2)  */
+  float eps_hi;       /* DAPO clip high (default 0.28) */
+  int32_t n_buckets;  /* per-turn buckets used (<= PRORL_TURN_BUCKETS) */
+  int32_t pad_;
+} prorl_loss_cfg;
+
+typedef struct prorl_score_cfg {
+  prorl_loss_cfg loss;
+  float inv_temperature; /* 1/SamplingParams::temperature (types.hpp:59) */
+  float adv_eps;         /* GRPO epsilon (1e-6) */
+  int32_t ddof;          /* GRPO std ddof (1) */
+  int32_t vocab;         /* V */
+  int32_t dtype;         /* prorl_dtype of logits */
+  int32_t microbatch_rows; /* active rows per logits micro-batch */
+} prorl_score_cfg;
+
+/* ---- context / errors ----------------------------------------------------- */
+int prorl_abi_version(void);
+const char* prorl_last_error(void);
+const char* prorl_status_code(int status); /* stable rollout::Error code string */
+int prorl_ctx_create(int device, prorl_ctx** out);
+int prorl_ctx_destroy(prorl_ctx* ctx);
+/* Synchronises `stream` and reports device-side validation failures raised by
+ * earlier calls on this ctx (token out of range, unsorted turns). */
+int prorl_check_errors(prorl_ctx* ctx, void* stream);
+
+/* ---- K1: pack ------------------------------------------------------------- */
+/* turns: device array [n_turns]; ids_dev/lp_dev: device flat wire arrays
+ * (int64 TokenId, fp64 logprob; lp entries of non-assistant turns ignored).
+ * n_tokens must equal sum(len) (host-known), n_seq = number of trajectories. */
+int prorl_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns,
+               const int64_t* ids_dev, const double* lp_dev, int64_t n_tokens,
+               int32_t n_seq, int32_t vocab, const prorl_packed* out, void* stream);
+
+/* ---- K3: GRPO advantages -------------------------------------------------- */
+/* reward: [n_rollouts] fp64, usable: [n_rollouts] (0 = FAILED), group_off:
+ * [n_groups+1] int32 rollout offsets. adv [n_rollouts] fp32 (0 for
+ * non-usable rollouts and non-informative groups), informative [n_groups].
+ * partials (nullable): adds sum(adv) and N_rollouts (usable rollouts of
+ * informative groups) into partials[8], partials[9]. */
+int prorl_grpo_adv(prorl_ctx* ctx, const double* reward, const uint8_t* usable,
+                   const int32_t* group_off, int32_t n_groups, int32_t ddof, float eps,
+                   double tolerance, float* adv, uint8_t* informative, double* partials,
+                   void* stream);
+
+/* ---- K2: logprob + entropy over the vocabulary ------------------------------ */
+/* logits: [*, row_stride] of dtype; row i of the call reads logits row
+ * rows[i] (rows may be NULL = identity). targets[i] in [0,V). */
+int prorl_logprob_entropy(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride,
+                          int32_t vocab, const int32_t* rows, const int32_t* targets,
+                          int64_t n_rows, float inv_temp, float* logp, float* entropy,
+                          void* stream);
+
+/* ---- K4: clipped surrogate + metrics -------------------------------------- */
+/* Adds this call's sums into partials_dev[PRORL_N_PARTIALS] (fp64) with a
+ * fixed reduction order (deterministic run to run). */
+int prorl_clipped_loss(prorl_ctx* ctx, const float* logp, const float* entropy,
+                       const float* old_lp, const float* adv, const int32_t* row_seq,
+                       const int16_t* row_turn, int64_t n_rows, const prorl_loss_cfg* cfg,
+                       double* partials_dev, void* stream);
+
+/* K2+K4 fused: one HBM pass per row and the loss epilogue in the same kernel.
+ * logp/entropy outputs are optional (may be NULL). */
+int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride,
+                     int32_t vocab, const int32_t* rows, const int32_t* targets,
+                     const float* old_lp, const float* adv, const int32_t* row_seq,
+                     const int16_t* row_turn, int64_t n_rows, float inv_temp,
+                     const prorl_loss_cfg* cfg, float* logp, float* entropy,
+                     double* partials_dev, void* stream);
+
+/* ---- NCCL ------------------------------------------------------------------ */
+/* 128-byte ncclUniqueId produced on rank 0, broadcast by the caller. */
+int prorl_nccl_unique_id(uint8_t* id128);
+int prorl_nccl_init(prorl_ctx* ctx, int nranks, int rank, const uint8_t* id128);
+/* In-place sum of partials_dev[n] over the ctx's communicator (no-op if
+ * nranks == 1 or no communicator). */
+int prorl_allreduce(prorl_ctx* ctx, double* partials_dev, int n, void* stream);
+
+/* ---- synthetic LM-head stand-in (bench / tests) ------------------------------ */
+/* Deterministic integer-hash logits, bit-identical to oracle/oracle.c
+ * (oracle_gen_logits): x[i][v] = bf16/fp32(2*sqrt(3)*sigma/2 * (u0+u1+u2+u3-2))
+ * and a planted target logit. row_key0 is the global index of row 0. */
+int prorl_gen_logits(prorl_ctx* ctx, void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                     int64_t n_rows, int64_t row_key0, const int32_t* targets,
+                     const float* old_lp, uint64_t seed, float sigma, void* stream);
+
+/* ---- host-side helpers ------------------------------------------------------ */
+/* Per-rollout rewards [num_prompts * n] with the semantics (and, under
+ * libstdc++, the exact values) of the reference's generate_workload
+ * (proj/src/trainer/workload.cpp:62-107), default latency options. */
+int prorl_synth_rewards(int32_t num_prompts, int32_t n, uint64_t seed, double p_informative, double* out);
+
+/* Deterministic LPT: groups sorted by load desc (tie: index asc) go to the
+ * least-loaded rank (tie: lowest rank). owner[g] in [0, world). */
+int prorl_shard_lpt(int32_t n_groups, const int64_t* load, int32_t world, int32_t* owner);
+
+/* Host SoA of one shard (all host pointers; pinned memory recommended). */
+typedef struct prorl_host_batch {
+  const prorl_turn_desc* turns; int64_t n_turns;
+  const int64_t* ids; const double* lp; int64_t n_tokens;
+  const double* reward; const uint8_t* usable; int32_t n_rollouts; /* = n_seq */
+  const int32_t* group_off; int32_t n_groups;
+} prorl_host_batch;
+
+/* Logits provider for prorl_score_host: micro-batch j (active rows
+ * [row0, row0+n)) reads logits from pool[j % n_pool] (each buffer holds
+ * >= microbatch_rows rows of row_stride elements). If `fill` is non-zero the
+ * library regenerates the buffer for micro-batch j with prorl_gen_logits
+ * before scoring it (parity mode; generation is then inside the call). */
+typedef struct prorl_logits_pool {
+  void* const* buffers; int32_t n_pool; int32_t fill; int64_t row_stride;
+  uint64_t seed; float sigma; int32_t pad_;
+} prorl_logits_pool;
+
+/* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for
+ * each micro-batch K2+K4 (fused), NCCL all-reduce (if initialised), D2H of
+ * the partials into host_partials[PRORL_N_PARTIALS]. Synchronises `stream`.
+ * timings_ms (nullable, [5]): h2d, pack+grpo, score (K2+K4 launches + slab
+ * reduce, incl. generation when pool->fill), allreduce, d2h. */
+int prorl_score_host(prorl_ctx* ctx, const prorl_host_batch* batch, const prorl_score_cfg* cfg,
+                     const prorl_logits_pool* logits, double* host_partials, float* timings_ms,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRORL_HOTPATH_H */

@@ -1,0 +1,399 @@
+// capi.cu — the extern "C" boundary declared in include/prorl_hotpath.h:
+// context/error plumbing, thin validated wrappers over the kernels, the NCCL
+// partials all-reduce, deterministic LPT group sharding, and prorl_score_host
+// (the whole per-GPU step from host buffers — the seam where the reference
+// drops the trajectory today, proj/src/trainer/harness.cpp:263-273).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace prorl {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("cuda_error: ") + cudaGetErrorString(e) + " in " + what;
+  return PRORL_E_CUDA;
+}
+
+// NCCL is resolved at run time from whichever libnccl.so.2 the process has
+// (torch brings its own); linking one at build time would clash with it.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool ok = false;
+};
+
+static const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_reduce && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+static int nccl_fail(ncclResult_t r, const char* what) {
+  g_last_error = std::string("nccl_error: ") + (nccl().error_string ? nccl().error_string(r) : "?") + " in " + what;
+  return PRORL_E_NCCL;
+}
+
+#define PRORL_NCCL_API()                                                                         \
+  do {                                                                                           \
+    if (!::prorl::nccl().ok) return ::prorl::fail(PRORL_E_NCCL, "nccl_error: libnccl.so.2 not loadable"); \
+  } while (0)
+
+#define PRORL_NCCL(call)                                   \
+  do {                                                     \
+    ncclResult_t r_ = (call);                              \
+    if (r_ != ncclSuccess) return ::prorl::nccl_fail(r_, #call); \
+  } while (0)
+
+#define PRORL_TRY(call)            \
+  do {                             \
+    int s_ = (call);               \
+    if (s_ != PRORL_OK) return s_; \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Host-side count of active rows: a policy token at position > 0 of its
+// sequence makes the previous row active.
+static int64_t host_active_rows(const prorl_turn_desc* turns, int64_t n_turns) {
+  int64_t n = 0;
+  int32_t cur = -1;
+  int64_t pos = 0;
+  for (int64_t t = 0; t < n_turns; ++t) {
+    if (turns[t].traj != cur) {
+      cur = turns[t].traj;
+      pos = 0;
+    }
+    if (turns[t].role == PRORL_ROLE_ASSISTANT && turns[t].len > 0) n += turns[t].len - (pos == 0 ? 1 : 0);
+    pos += turns[t].len;
+  }
+  return n;
+}
+
+}  // namespace prorl
+
+using namespace prorl;
+
+extern "C" {
+
+int prorl_abi_version(void) { return PRORL_ABI_VERSION; }
+
+const char* prorl_last_error(void) { return g_last_error.c_str(); }
+
+const char* prorl_status_code(int status) {
+  switch (status) {
+    case PRORL_OK: return "ok";
+    case PRORL_E_MALFORMED_TURN: return "malformed_turn";
+    case PRORL_E_INCOMPLETE_GROUP: return "incomplete_group";
+    case PRORL_E_MALFORMED_REQUEST: return "malformed_request";
+    case PRORL_E_CUDA: return "cuda_error";
+    case PRORL_E_NCCL: return "nccl_error";
+    case PRORL_E_SHAPE: return "shape_mismatch";
+    case PRORL_E_TOKEN_RANGE: return "shape_mismatch";
+  }
+  return "unknown";
+}
+
+int prorl_ctx_create(int device, prorl_ctx** out) {
+  if (!out) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_ctx_create: out is null");
+  *out = nullptr;
+  PRORL_CUDA(cudaSetDevice(device));
+  prorl_ctx* c = new prorl_ctx();
+  c->device = device;
+  cudaError_t e = cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(int) * ERR_N);
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int) * ERR_N);
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "prorl_ctx_create");
+  }
+  *out = c;
+  return PRORL_OK;
+}
+
+int prorl_ctx_destroy(prorl_ctx* c) {
+  if (!c) return PRORL_OK;
+  cudaSetDevice(c->device);
+  if (c->nccl_comm && nccl().ok) nccl().comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
+  for (auto* b : {&c->scan_tmp, &c->pack_tmp, &c->slab, &c->grpo_tmp, &c->h_turns, &c->h_ids, &c->h_lp,
+                  &c->h_reward, &c->h_usable, &c->h_goff, &c->p_tokens, &c->p_mask, &c->p_turn, &c->p_seq,
+                  &c->p_pos, &c->p_cu, &c->p_oldlp, &c->a_row, &c->a_target, &c->a_oldlp, &c->a_seq, &c->a_turn,
+                  &c->a_nact, &c->adv, &c->informative, &c->partials, &c->logp, &c->entropy})
+    b->release();
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->d_err) cudaFree(c->d_err);
+  delete c;
+  return PRORL_OK;
+}
+
+int prorl_check_errors(prorl_ctx* c, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "null ctx");
+  int h[ERR_N] = {0};
+  PRORL_CUDA(cudaStreamSynchronize(S(stream)));
+  PRORL_CUDA(cudaMemcpy(h, c->d_err, sizeof(h), cudaMemcpyDeviceToHost));
+  PRORL_CUDA(cudaMemset(c->d_err, 0, sizeof(h)));
+  if (h[ERR_TOKEN_RANGE]) return fail(PRORL_E_TOKEN_RANGE, "shape_mismatch: token id outside [0, vocab)");
+  if (h[ERR_TURN_ORDER])
+    return fail(PRORL_E_SHAPE, "shape_mismatch: turn descriptors not sorted by traj / traj outside [0, n_seq) / bad role");
+  if (h[ERR_TOKEN_COUNT]) return fail(PRORL_E_SHAPE, "shape_mismatch: n_tokens != sum of turn lengths");
+  return PRORL_OK;
+}
+
+int prorl_pack(prorl_ctx* c, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids, const double* lp,
+               int64_t n_tokens, int32_t n_seq, int32_t vocab, const prorl_packed* out, void* stream) {
+  if (!c || !out) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_pack: null ctx/out");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_pack(c, turns, n_turns, ids, lp, n_tokens, n_seq, vocab, out, S(stream));
+}
+
+int prorl_grpo_adv(prorl_ctx* c, const double* reward, const uint8_t* usable, const int32_t* group_off,
+                   int32_t n_groups, int32_t ddof, float eps, double tolerance, float* adv, uint8_t* informative,
+                   double* partials, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_grpo_adv: null ctx");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_grpo(c, reward, usable, group_off, n_groups, ddof, eps, tolerance, adv, informative, partials,
+                     S(stream));
+}
+
+int prorl_logprob_entropy(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                          const int32_t* rows, const int32_t* targets, int64_t n_rows, float inv_temp, float* logp,
+                          float* entropy, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_logprob_entropy: null ctx");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_score(c, logits, dtype, row_stride, vocab, rows, targets, nullptr, nullptr, nullptr, nullptr, n_rows,
+                      inv_temp, nullptr, logp, entropy, nullptr, 0, false, nullptr, S(stream));
+}
+
+int prorl_clipped_loss(prorl_ctx* c, const float* logp, const float* entropy, const float* old_lp, const float* adv,
+                       const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, const prorl_loss_cfg* cfg,
+                       double* partials_dev, void* stream) {
+  if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_clipped_loss: null ctx/cfg");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  const int rows = loss_slab_rows(c);
+  PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(rows, score_slab_rows(c))));
+  int used = 0;
+  PRORL_TRY(launch_loss(c, logp, entropy, old_lp, adv, row_seq, row_turn, n_rows, cfg, c->slab.as<double>(), rows,
+                        &used, S(stream)));
+  return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
+}
+
+int prorl_score_rows(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                     const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                     const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, float inv_temp,
+                     const prorl_loss_cfg* cfg, float* logp, float* entropy, double* partials_dev, void* stream) {
+  if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_rows: null ctx/cfg");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  const int srows = score_slab_rows(c);
+  PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(srows, loss_slab_rows(c))));
+  int used = 0;
+  PRORL_TRY(launch_score(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, n_rows,
+                         inv_temp, cfg, logp, entropy, c->slab.as<double>(), srows, false, &used, S(stream)));
+  return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
+}
+
+int prorl_nccl_unique_id(uint8_t* id128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  PRORL_NCCL_API();
+  ncclUniqueId id;
+  PRORL_NCCL(nccl().get_unique_id(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return PRORL_OK;
+}
+
+int prorl_nccl_init(prorl_ctx* c, int nranks, int rank, const uint8_t* id128) {
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_nccl_init: bad args");
+  PRORL_NCCL_API();
+  PRORL_CUDA(cudaSetDevice(c->device));
+  if (c->nccl_comm) {
+    nccl().comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
+    c->nccl_comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t comm;
+  PRORL_NCCL(nccl().comm_init_rank(&comm, nranks, id, rank));
+  c->nccl_comm = comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  return PRORL_OK;
+}
+
+int prorl_allreduce(prorl_ctx* c, double* partials_dev, int n, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_allreduce: null ctx");
+  if (!c->nccl_comm || c->nranks == 1 || n <= 0) return PRORL_OK;
+  PRORL_CUDA(cudaSetDevice(c->device));
+  PRORL_NCCL(nccl().all_reduce(partials_dev, partials_dev, (size_t)n, ncclDouble, ncclSum,
+                           static_cast<ncclComm_t>(c->nccl_comm), S(stream)));
+  return PRORL_OK;
+}
+
+int prorl_gen_logits(prorl_ctx* c, void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
+                     int64_t row_key0, const int32_t* targets, const float* old_lp, uint64_t seed, float sigma,
+                     void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_gen_logits: null ctx");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  const float scale = (float)((double)sigma * std::sqrt(3.0));
+  const float base = (float)(std::log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
+  return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, row_key0, targets, old_lp, seed, scale, base,
+                           c->n_sm, S(stream));
+}
+
+int prorl_shard_lpt(int32_t n_groups, const int64_t* load, int32_t world, int32_t* owner) {
+  if (n_groups < 0 || world < 1 || (n_groups > 0 && (!load || !owner)))
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_shard_lpt: bad args");
+  std::vector<int32_t> order(n_groups);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return load[a] > load[b]; });
+  std::vector<int64_t> acc(world, 0);
+  for (int32_t g : order) {
+    int32_t best = 0;
+    for (int32_t r = 1; r < world; ++r)
+      if (acc[r] < acc[best]) best = r;
+    owner[g] = best;
+    acc[best] += load[g];
+  }
+  return PRORL_OK;
+}
+
+int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_cfg* cfg,
+                     const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream) {
+  if (!c || !hb || !cfg || !pool || !host_partials)
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null argument");
+  if (pool->n_pool < 1 || !pool->buffers) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: empty logits pool");
+  if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
+  if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
+    return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
+  if (hb->n_groups > 0 && hb->group_off[hb->n_groups] != hb->n_rollouts)
+    return fail(PRORL_E_SHAPE, "prorl_score_host: group_off[n_groups] != n_rollouts");
+  int64_t tok = 0;
+  for (int64_t t = 0; t < hb->n_turns; ++t) tok += hb->turns[t].len;
+  if (tok != hb->n_tokens) return fail(PRORL_E_SHAPE, "prorl_score_host: n_tokens != sum of turn lengths");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = S(stream);
+  const int64_t N = hb->n_tokens, A = host_active_rows(hb->turns, hb->n_turns);
+  const int32_t R = hb->n_rollouts, G = hb->n_groups;
+  const int srows = score_slab_rows(c);
+
+  // device staging (grown on demand, kept across calls)
+  PRORL_CUDA(c->h_turns.ensure(sizeof(prorl_turn_desc) * (size_t)std::max<int64_t>(hb->n_turns, 1)));
+  PRORL_CUDA(c->h_ids.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->h_lp.ensure(sizeof(double) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->h_reward.ensure(sizeof(double) * (size_t)std::max(R, 1)));
+  PRORL_CUDA(c->h_usable.ensure((size_t)std::max(R, 1)));
+  PRORL_CUDA(c->h_goff.ensure(sizeof(int32_t) * (size_t)(G + 1)));
+  PRORL_CUDA(c->p_tokens.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->p_mask.ensure((size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->p_turn.ensure(sizeof(int16_t) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->p_seq.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->p_pos.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->p_cu.ensure(sizeof(int32_t) * (size_t)(R + 1)));
+  PRORL_CUDA(c->p_oldlp.ensure(sizeof(float) * (size_t)std::max<int64_t>(N, 1)));
+  PRORL_CUDA(c->a_row.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(A, 1)));
+  PRORL_CUDA(c->a_target.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(A, 1)));
+  PRORL_CUDA(c->a_oldlp.ensure(sizeof(float) * (size_t)std::max<int64_t>(A, 1)));
+  PRORL_CUDA(c->a_seq.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(A, 1)));
+  PRORL_CUDA(c->a_turn.ensure(sizeof(int16_t) * (size_t)std::max<int64_t>(A, 1)));
+  PRORL_CUDA(c->a_nact.ensure(sizeof(int64_t)));
+  PRORL_CUDA(c->adv.ensure(sizeof(float) * (size_t)std::max(R, 1)));
+  PRORL_CUDA(c->informative.ensure((size_t)std::max(G, 1)));
+  PRORL_CUDA(c->partials.ensure(sizeof(double) * PRORL_N_PARTIALS));
+  PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(srows, loss_slab_rows(c))));
+
+  double* partials = c->partials.as<double>();
+  double* slab = c->slab.as<double>();
+  PRORL_CUDA(cudaEventRecord(c->ev[0], st));
+  // ---- H2D ----
+  if (hb->n_turns)
+    PRORL_CUDA(cudaMemcpyAsync(c->h_turns.p, hb->turns, sizeof(prorl_turn_desc) * hb->n_turns, cudaMemcpyHostToDevice, st));
+  if (N) {
+    PRORL_CUDA(cudaMemcpyAsync(c->h_ids.p, hb->ids, sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
+    PRORL_CUDA(cudaMemcpyAsync(c->h_lp.p, hb->lp, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  }
+  if (R) {
+    PRORL_CUDA(cudaMemcpyAsync(c->h_reward.p, hb->reward, sizeof(double) * R, cudaMemcpyHostToDevice, st));
+    PRORL_CUDA(cudaMemcpyAsync(c->h_usable.p, hb->usable, (size_t)R, cudaMemcpyHostToDevice, st));
+  }
+  if (G) PRORL_CUDA(cudaMemcpyAsync(c->h_goff.p, hb->group_off, sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, st));
+  PRORL_CUDA(cudaMemsetAsync(partials, 0, sizeof(double) * PRORL_N_PARTIALS, st));
+  PRORL_CUDA(cudaMemsetAsync(slab, 0, sizeof(double) * PRORL_N_PARTIALS * srows, st));
+  PRORL_CUDA(cudaEventRecord(c->ev[1], st));
+
+  // ---- K1 pack, K3 grpo ----
+  prorl_packed pk{};
+  pk.tokens = c->p_tokens.as<int32_t>();
+  pk.loss_mask = c->p_mask.as<uint8_t>();
+  pk.turn_id = c->p_turn.as<int16_t>();
+  pk.seq_id = c->p_seq.as<int32_t>();
+  pk.pos_id = c->p_pos.as<int32_t>();
+  pk.cu_seqlens = c->p_cu.as<int32_t>();
+  pk.old_lp = c->p_oldlp.as<float>();
+  pk.act_row = c->a_row.as<int32_t>();
+  pk.act_target = c->a_target.as<int32_t>();
+  pk.act_old_lp = c->a_oldlp.as<float>();
+  pk.act_seq = c->a_seq.as<int32_t>();
+  pk.act_turn = c->a_turn.as<int16_t>();
+  pk.n_active = c->a_nact.as<int64_t>();
+  PRORL_TRY(launch_pack(c, c->h_turns.as<prorl_turn_desc>(), hb->n_turns, c->h_ids.as<int64_t>(),
+                        c->h_lp.as<double>(), N, R, cfg->vocab, &pk, st));
+  PRORL_TRY(launch_grpo(c, c->h_reward.as<double>(), c->h_usable.as<uint8_t>(), c->h_goff.as<int32_t>(), G, cfg->ddof,
+                        cfg->adv_eps, 0.0, c->adv.as<float>(), c->informative.as<uint8_t>(), partials, st));
+  PRORL_CUDA(cudaEventRecord(c->ev[2], st));
+
+  // ---- K2+K4 over logits micro-batches ----
+  const int64_t mb = cfg->microbatch_rows;
+  for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
+    const int64_t n = std::min(mb, A - row0);
+    void* buf = pool->buffers[j % pool->n_pool];
+    if (pool->fill)
+      PRORL_TRY(prorl_gen_logits(c, buf, cfg->dtype, pool->row_stride, cfg->vocab, n, row0, pk.act_target + row0,
+                                 pk.act_old_lp + row0, pool->seed, pool->sigma, st));
+    PRORL_TRY(launch_score(c, buf, cfg->dtype, pool->row_stride, cfg->vocab, nullptr, pk.act_target + row0,
+                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, n,
+                           cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
+  }
+  PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
+  PRORL_CUDA(cudaEventRecord(c->ev[3], st));
+  PRORL_TRY(prorl_allreduce(c, partials, PRORL_N_PARTIALS, stream));
+  PRORL_CUDA(cudaEventRecord(c->ev[4], st));
+  PRORL_CUDA(cudaMemcpyAsync(host_partials, partials, sizeof(double) * PRORL_N_PARTIALS, cudaMemcpyDeviceToHost, st));
+  PRORL_CUDA(cudaEventRecord(c->ev[5], st));
+  PRORL_TRY(prorl_check_errors(c, stream));
+  if (timings_ms) {
+    for (int k = 0; k < 5; ++k) PRORL_CUDA(cudaEventElapsedTime(&timings_ms[k], c->ev[k], c->ev[k + 1]));
+  }
+  return PRORL_OK;
+}
+
+}  // extern "C"

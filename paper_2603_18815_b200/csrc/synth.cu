@@ -1,0 +1,57 @@
+// synth.cu — deterministic synthetic LM-head output (stand-in for the model
+// forward, out of the reference's scope: SPEC.md:8). The value of every
+// element is defined in include/prorl_synth.h and is bit-identical to the CPU
+// oracle's oracle_gen_logits. Not on the timed path of the benchmark.
+#include "common.cuh"
+#include "prorl_synth.h"
+
+namespace prorl {
+
+namespace {
+
+template <bool BF16>
+__global__ void k_gen_logits(uint8_t* __restrict__ out, int64_t row_stride, int32_t vocab, int64_t n_rows,
+                             int64_t row_key0, const int32_t* __restrict__ targets,
+                             const float* __restrict__ old_lp, uint32_t s0, float scale, float base) {
+  const int64_t total = n_rows * (int64_t)vocab;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / vocab;
+    const int32_t col = (int32_t)(idx - i * vocab);
+    const uint64_t row_key = (uint64_t)(row_key0 + i);
+    float x;
+    if (old_lp != nullptr && targets[i] == col)
+      x = prorl_plant_logit(row_key, s0, base, old_lp[i]);
+    else
+      x = prorl_noise_logit(row_key * (uint64_t)vocab + (uint64_t)col, s0, scale);
+    const int64_t o = i * row_stride + col;
+    if (BF16) {
+      reinterpret_cast<uint16_t*>(out)[o] = prorl_f32_to_bf16_bits(x);
+    } else {
+      reinterpret_cast<float*>(out)[o] = x;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows, int64_t row_key0,
+                      const int32_t* targets, const float* old_lp, uint64_t seed, float scale, float base, int n_sm,
+                      cudaStream_t st) {
+  if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "gen_logits: unknown dtype");
+  if (vocab <= 0 || row_stride < vocab || n_rows < 0) return fail(PRORL_E_SHAPE, "gen_logits: bad shape");
+  if (old_lp && !targets) return fail(PRORL_E_SHAPE, "gen_logits: old_lp given without targets");
+  if (n_rows == 0) return PRORL_OK;
+  const uint32_t s0 = prorl_seed_mix(seed);
+  const int grid = n_sm * 8;
+  if (dtype == PRORL_BF16)
+    k_gen_logits<true><<<grid, 512, 0, st>>>(static_cast<uint8_t*>(logits), row_stride, vocab, n_rows, row_key0,
+                                             targets, old_lp, s0, scale, base);
+  else
+    k_gen_logits<false><<<grid, 512, 0, st>>>(static_cast<uint8_t*>(logits), row_stride, vocab, n_rows, row_key0,
+                                              targets, old_lp, s0, scale, base);
+  PRORL_CUDA(cudaGetLastError());
+  return PRORL_OK;
+}
+
+}  // namespace prorl

@@ -1,0 +1,252 @@
+"""Python handle over the C-ABI (include/prorl_hotpath.h) for tests and the bench.
+
+The product is the C/C++ library; this module only moves torch device
+pointers / numpy host pointers across ctypes and maps status codes onto
+`RolloutError` (the rollout::Error code convention, errors.hpp:10-18).
+Every call runs the sm_100a kernels; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import check, ptr
+
+_DT = {torch.bfloat16: N.PRORL_BF16, torch.float32: N.PRORL_FP32}
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class LossConfig:
+    eps_lo: float = 0.2
+    eps_hi: float = 0.28
+    n_buckets: int = N.TURN_BUCKETS
+
+    def c(self) -> N.LossCfg:
+        return N.LossCfg(self.eps_lo, self.eps_hi, self.n_buckets, 0)
+
+
+@dataclass
+class ScoreConfig:
+    """Mirror of the C++ rollout::train::ScoreConfig."""
+    vocab: int
+    dtype: str = "bf16"
+    inv_temperature: float = 1.0
+    adv_eps: float = 1e-6
+    ddof: int = 1
+    microbatch_rows: int = 16384
+    loss: LossConfig = None
+
+    def c(self) -> N.ScoreCfg:
+        loss = self.loss or LossConfig()
+        return N.ScoreCfg(loss.c(), self.inv_temperature, self.adv_eps, self.ddof, self.vocab,
+                          N.PRORL_BF16 if self.dtype == "bf16" else N.PRORL_FP32, self.microbatch_rows)
+
+
+class Scorer:
+    """One prorl_ctx on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        check(N.lib.prorl_ctx_create(device, C.byref(h)))
+        self.ctx = h
+
+    def close(self) -> None:
+        if self.ctx:
+            N.lib.prorl_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check_errors(self, stream=None) -> None:
+        check(N.lib.prorl_check_errors(self.ctx, _stream(stream)))
+
+    # ---- K1 ----
+    def pack(self, turns: np.ndarray, ids: torch.Tensor, lp: torch.Tensor, n_seq: int, vocab: int,
+             n_active: int, stream=None) -> dict:
+        dev = ids.device
+        n_tok = ids.numel()
+        t_dev = torch.from_numpy(turns.view(np.uint8).reshape(-1)).to(dev)
+        e = lambda n, dt: torch.empty(max(n, 1), dtype=dt, device=dev)
+        out = {
+            "tokens": e(n_tok, torch.int32), "loss_mask": e(n_tok, torch.uint8), "turn_id": e(n_tok, torch.int16),
+            "seq_id": e(n_tok, torch.int32), "pos_id": e(n_tok, torch.int32), "cu_seqlens": e(n_seq + 1, torch.int32),
+            "old_lp": e(n_tok, torch.float32), "act_row": e(n_active, torch.int32),
+            "act_target": e(n_active, torch.int32), "act_old_lp": e(n_active, torch.float32),
+            "act_seq": e(n_active, torch.int32), "act_turn": e(n_active, torch.int16),
+            "n_active": torch.zeros(1, dtype=torch.int64, device=dev),
+        }
+        pk = N.Packed(*[ptr(out[f]) for f, _ in N.Packed._fields_])
+        check(N.lib.prorl_pack(self.ctx, ptr(t_dev), len(turns), ptr(ids), ptr(lp), n_tok, n_seq, vocab,
+                               C.byref(pk), _stream(stream)))
+        self.check_errors(stream)
+        for k in ("tokens", "loss_mask", "turn_id", "seq_id", "pos_id", "old_lp"):
+            out[k] = out[k][:n_tok]
+        for k in ("act_row", "act_target", "act_old_lp", "act_seq", "act_turn"):
+            out[k] = out[k][:n_active]
+        return out
+
+    # ---- K3 ----
+    def grpo_adv(self, reward: torch.Tensor, usable: torch.Tensor, group_off: torch.Tensor, ddof: int = 1,
+                 eps: float = 1e-6, tol: float = 0.0, partials: torch.Tensor | None = None, stream=None):
+        adv = torch.empty(max(reward.numel(), 1), dtype=torch.float32, device=reward.device)
+        ng = group_off.numel() - 1
+        info = torch.empty(max(ng, 1), dtype=torch.uint8, device=reward.device)
+        check(N.lib.prorl_grpo_adv(self.ctx, ptr(reward), ptr(usable), ptr(group_off), ng, ddof, eps, tol, ptr(adv),
+                                   ptr(info), ptr(partials), _stream(stream)))
+        return adv[:reward.numel()], info[:ng]
+
+    # ---- K2 ----
+    def logprob_entropy(self, logits: torch.Tensor, targets: torch.Tensor, rows: torch.Tensor | None = None,
+                        inv_temp: float = 1.0, vocab: int | None = None, stream=None):
+        n = targets.numel()
+        logp = torch.empty(n, dtype=torch.float32, device=targets.device)
+        ent = torch.empty(n, dtype=torch.float32, device=targets.device)
+        V = vocab if vocab is not None else logits.shape[1]
+        check(N.lib.prorl_logprob_entropy(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
+                                          ptr(targets), n, inv_temp, ptr(logp), ptr(ent), _stream(stream)))
+        return logp, ent
+
+    # ---- K4 ----
+    def clipped_loss(self, logp, entropy, old_lp, adv, row_seq, row_turn, cfg: LossConfig | None = None,
+                     partials: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if partials is None:
+            partials = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=logp.device)
+        c = (cfg or LossConfig()).c()
+        check(N.lib.prorl_clipped_loss(self.ctx, ptr(logp), ptr(entropy), ptr(old_lp), ptr(adv), ptr(row_seq),
+                                       ptr(row_turn), logp.numel(), C.byref(c), ptr(partials), _stream(stream)))
+        return partials
+
+    # ---- K2+K4 fused ----
+    def score_rows(self, logits, targets, old_lp, adv, row_seq, row_turn, rows=None, inv_temp: float = 1.0,
+                   cfg: LossConfig | None = None, partials=None, want_rows: bool = True, vocab: int | None = None,
+                   stream=None):
+        n = targets.numel()
+        dev = targets.device
+        if partials is None:
+            partials = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=dev)
+        logp = torch.empty(n, dtype=torch.float32, device=dev) if want_rows else None
+        ent = torch.empty(n, dtype=torch.float32, device=dev) if want_rows else None
+        c = (cfg or LossConfig()).c()
+        V = vocab if vocab is not None else logits.shape[1]
+        check(N.lib.prorl_score_rows(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
+                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), n, inv_temp,
+                                     C.byref(c), ptr(logp), ptr(ent), ptr(partials), _stream(stream)))
+        return partials, logp, ent
+
+    # ---- synthetic LM head ----
+    def gen_logits(self, out: torch.Tensor, n_rows: int, row_key0: int, targets=None, old_lp=None, seed: int = 0,
+                   sigma: float = 2.0, vocab: int | None = None, stream=None) -> torch.Tensor:
+        V = vocab if vocab is not None else out.shape[1]
+        check(N.lib.prorl_gen_logits(self.ctx, ptr(out), _DT[out.dtype], out.stride(0), V, n_rows, row_key0,
+                                     ptr(targets), ptr(old_lp), seed, sigma, _stream(stream)))
+        return out
+
+    # ---- NCCL ----
+    def nccl_init(self, world: int, rank: int, uid: bytes) -> None:
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(N.lib.prorl_nccl_init(self.ctx, world, rank, C.addressof(buf)))
+
+    def allreduce(self, partials: torch.Tensor, stream=None) -> None:
+        check(N.lib.prorl_allreduce(self.ctx, ptr(partials), partials.numel(), _stream(stream)))
+
+    # ---- whole per-GPU step from host buffers ----
+    def score_host(self, batch: "HostBatchArrays", cfg: ScoreConfig, pool: list[torch.Tensor], fill: bool,
+                   seed: int = 0, sigma: float = 2.0, stream=None):
+        hb = batch.c()
+        bufs = (C.c_void_p * len(pool))(*[ptr(b) for b in pool])
+        lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0)
+        out = np.zeros(N.N_PARTIALS, dtype=np.float64)
+        tm = np.zeros(5, dtype=np.float32)
+        sc = cfg.c()
+        check(N.lib.prorl_score_host(self.ctx, C.byref(hb), C.byref(sc), C.byref(lp), ptr(out), ptr(tm),
+                                     _stream(stream)))
+        return out, tm
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(N.lib.prorl_nccl_unique_id(C.addressof(buf)))
+    return bytes(buf)
+
+
+def shard_lpt(load: np.ndarray, world: int) -> np.ndarray:
+    load = np.ascontiguousarray(load, dtype=np.int64)
+    owner = np.zeros(len(load), dtype=np.int32)
+    check(N.lib.prorl_shard_lpt(len(load), ptr(load), world, ptr(owner)))
+    return owner
+
+
+def synth_rewards(num_prompts: int, n: int, seed: int, p_informative: float = 0.5) -> np.ndarray:
+    out = np.zeros(num_prompts * n, dtype=np.float64)
+    check(N.lib.prorl_synth_rewards(num_prompts, n, seed, p_informative, ptr(out)))
+    return out.reshape(num_prompts, n)
+
+
+@dataclass
+class HostBatchArrays:
+    """Host SoA of one shard (prorl_host_batch). Arrays must stay alive."""
+    turns: np.ndarray      # TURN_DTYPE
+    ids: np.ndarray        # int64 wire TokenIds (types.hpp:12)
+    lp: np.ndarray         # float64 wire logprobs (trajectory.hpp:31)
+    reward: np.ndarray     # float64 per rollout slot
+    usable: np.ndarray     # uint8 per rollout slot (0 = FAILED)
+    group_off: np.ndarray  # int32 [n_groups+1]
+
+    def c(self) -> N.HostBatch:
+        return N.HostBatch(ptr(self.turns), len(self.turns), ptr(self.ids), ptr(self.lp), len(self.ids),
+                           ptr(self.reward), ptr(self.usable), len(self.reward), ptr(self.group_off),
+                           len(self.group_off) - 1)
+
+    def pinned(self) -> "HostBatchArrays":
+        """Copy into page-locked host memory (torch pinned tensors)."""
+        def pin(a):
+            t = torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1)).pin_memory()
+            return t.numpy().view(a.dtype).reshape(a.shape)
+        return HostBatchArrays(*(pin(getattr(self, f)) for f in
+                                 ("turns", "ids", "lp", "reward", "usable", "group_off")))
+
+    @property
+    def n_tokens(self) -> int:
+        return len(self.ids)
+
+    @property
+    def n_rollouts(self) -> int:
+        return len(self.reward)
+
+    @property
+    def n_groups(self) -> int:
+        return len(self.group_off) - 1
+
+    def bytes_h2d(self) -> int:
+        return sum(getattr(self, f).nbytes for f in ("turns", "ids", "lp", "reward", "usable", "group_off"))
+
+
+def finalize(p: np.ndarray) -> dict:
+    """Host-side finalisation of the all-reduced partials."""
+    n = max(p[N.P_N_ACTIVE], 1.0)
+    out = {
+        "loss": p[N.P_LOSS_SUM] / n, "n_active": int(p[N.P_N_ACTIVE]), "entropy": p[N.P_ENTROPY_SUM] / n,
+        "logp": p[N.P_LOGP_SUM] / n, "ratio": p[N.P_RATIO_SUM] / n, "clip_lo_frac": p[N.P_CLIP_LO] / n,
+        "clip_hi_frac": p[N.P_CLIP_HI] / n, "kl_k1": p[N.P_KL1_SUM] / n, "adv_sum": p[N.P_ADV_SUM],
+        "n_rollouts": int(p[N.P_N_ROLLOUTS]),
+    }
+    per_turn = p[N.N_GLOBAL:].reshape(N.TURN_BUCKETS, N.N_PER_TURN)
+    out["per_turn"] = [
+        {"turn": k, "n": int(r[0]), "loss": r[1] / max(r[0], 1), "entropy": r[2] / max(r[0], 1),
+         "logp": r[3] / max(r[0], 1), "clip_frac": r[4] / max(r[0], 1)}
+        for k, r in enumerate(per_turn) if r[0] > 0]
+    return out

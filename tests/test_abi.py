@@ -1,0 +1,78 @@
+"""C-ABI surface (no GPU): the library loads, exports every function
+include/prorl_hotpath.h declares, and the host-only entry points behave."""
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2603_18815_b200 import _native as N
+from paper_2603_18815_b200.hotpath import shard_lpt, synth_rewards
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "prorl_hotpath.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(prorl_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported():
+    decl = declared_functions()
+    assert len(decl) >= 18
+    missing = [f for f in decl if not hasattr(N.lib, f)]
+    assert not missing, missing
+    assert sorted(N.EXPORTS) == decl
+
+
+def test_abi_version_and_codes():
+    assert N.lib.prorl_abi_version() == 1
+    assert N.lib.prorl_status_code(-1) == b"malformed_turn"
+    assert N.lib.prorl_status_code(-2) == b"incomplete_group"
+    assert N.lib.prorl_status_code(-10) == b"cuda_error"
+    assert N.lib.prorl_status_code(-11) == b"nccl_error"
+    assert N.lib.prorl_status_code(-12) == b"shape_mismatch"
+
+
+def test_struct_layouts_match_header():
+    import ctypes as C
+    assert C.sizeof(N.Packed) == 13 * 8
+    assert C.sizeof(N.LossCfg) == 16
+    assert C.sizeof(N.ScoreCfg) == 40
+    assert N.TURN_DTYPE.itemsize == 24
+    assert C.sizeof(N.HostBatch) == 80
+    assert C.sizeof(N.LogitsPool) == 40
+
+
+def test_shard_lpt_deterministic_and_balanced():
+    load = np.array([5, 9, 2, 9, 7, 1, 3, 3], np.int64)
+    owner = shard_lpt(load, 3)
+    # LPT: desc load (ties by index): 9(g1)->r0, 9(g3)->r1, 7(g4)->r2, 5(g0)->r2 (7<9? no: r2=7 is least) ...
+    acc = np.zeros(3, np.int64)
+    order = sorted(range(len(load)), key=lambda g: (-load[g], g))
+    want = np.zeros(len(load), np.int32)
+    for g in order:
+        r = int(np.argmin(acc))
+        want[g] = r
+        acc[r] += load[g]
+    assert owner.tolist() == want.tolist()
+    assert shard_lpt(load, 3).tolist() == owner.tolist()
+    assert shard_lpt(load, 1).tolist() == [0] * len(load)
+
+
+def test_synth_rewards_semantics():
+    r = synth_rewards(200, 8, 2604, 0.5)
+    assert set(np.unique(r)) <= {0.0, 1.0}
+    mixed = [(row.min() != row.max()) for row in r]
+    # informative groups have 1..n-1 successes (workload.cpp:86-94)
+    assert 0.3 < np.mean(mixed) < 0.7
+    for row in r:
+        if row.min() != row.max():
+            assert 1 <= row.sum() <= 7
+
+
+def test_error_code_for_bad_request():
+    with pytest.raises(N.RolloutError) as e:
+        N.check(N.lib.prorl_synth_rewards(0, 4, 0, 0.5, None))
+    assert e.value.code == "malformed_request"

@@ -1,0 +1,169 @@
+"""Pin the CPU oracle against the reference: its own test KATs (restated from
+proj/tests/*.cpp) and golden vectors produced by the compiled reference
+(tests/golden/reference_vectors.json, made by tests/golden/make_golden.py)."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2603_18815_b200 import _native as N
+
+GOLD = json.loads((Path(__file__).parent / "golden" / "reference_vectors.json").read_text())
+L = O.lib()
+
+
+def _turns(roles, lens):
+    t = np.zeros(len(roles), dtype=N.TURN_DTYPE)
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]) if len(lens) else []
+    t["src_off"], t["traj"], t["len"], t["role"] = off, 0, lens, roles
+    return t
+
+
+# ---- test_core.cpp:130-142: flatten order golden -------------------------------
+def test_flatten_kat_test_core():
+    roles = [N.ROLE_USER, N.ROLE_ASSISTANT, N.ROLE_TOOL, N.ROLE_ASSISTANT]
+    lens = [3, 2, 1, 1]
+    ids = np.array([1, 2, 3, 10, 11, 4, 12], np.int64)
+    r = np.array(roles, np.int32)
+    l = np.array(lens, np.int64)
+    out = np.zeros(16, np.int64)
+
+    def fr(b, e):
+        n = L.oracle_flatten(4, r.ctypes.data, l.ctypes.data, ids.ctypes.data, b, e, out.ctypes.data, 16)
+        return out[:n].tolist()
+
+    assert fr(0, 4) == [1, 2, 3, 10, 11, 4, 12]
+    assert fr(1, 3) == [10, 11, 4]
+    assert fr(3, 99) == [12]
+    assert fr(2, 2) == []
+    # the packer on the same trajectory: order + the derived mask [0,0,0,1,1,0,1]
+    lp = np.array([0, 0, 0, -1.0, -1.1, 0, -1.2])
+    st, pk = O.pack(_turns(roles, lens), ids, lp, 1, 50000)
+    assert st == 0
+    assert pk["tokens"].tolist() == [1, 2, 3, 10, 11, 4, 12]
+    assert pk["loss_mask"].tolist() == [0, 0, 0, 1, 1, 0, 1]
+    assert pk["turn_id"].tolist() == [-1, -1, -1, 0, 0, -1, 1]
+    assert pk["cu_seqlens"].tolist() == [0, 7]
+    # active rows: r such that token r+1 is a policy token -> rows 2, 3, 5
+    assert pk["act_row"].tolist() == [2, 3, 5]
+    assert pk["act_target"].tolist() == [10, 11, 12]
+    np.testing.assert_array_equal(pk["act_old_lp"], np.float32([-1.0, -1.1, -1.2]))
+
+
+# ---- test_core.cpp:144-170: malformed turns -------------------------------------
+@pytest.mark.parametrize("role,ni,no,nl", [(N.ROLE_ASSISTANT, 1, 0, 0), (N.ROLE_ASSISTANT, 0, 2, 1),
+                                           (N.ROLE_USER, 0, 1, 0), (N.ROLE_TOOL, 0, 0, 1)])
+def test_malformed_turn_kat(role, ni, no, nl):
+    assert L.oracle_validate_turn(role, ni, no, nl) == 1
+
+
+def test_wellformed_turns():
+    assert L.oracle_validate_turn(N.ROLE_ASSISTANT, 0, 2, 2) == 0
+    assert L.oracle_validate_turn(N.ROLE_USER, 3, 0, 0) == 0
+
+
+# ---- test_trainer.cpp:148-166: informative filter -------------------------------
+def _inf(rewards, failed=None, has=None, tol=0.0):
+    n = len(rewards)
+    h = np.array(has if has is not None else [1] * n, np.int32)
+    f = np.array(failed if failed is not None else [0] * n, np.int32)
+    w = np.array(rewards, np.float64)
+    return L.oracle_is_informative(n, h.ctypes.data, f.ctypes.data, w.ctypes.data, tol)
+
+
+def test_informative_kat_test_trainer():
+    assert _inf([1, 1, 1, 1]) == 0
+    assert _inf([1, 0, 1, 1]) == 1
+    assert _inf([1, 1, 0, 1], failed=[0, 0, 1, 0]) == 0
+    assert _inf([1, 0], failed=[0, 1]) == 0
+    assert _inf([0.0, 0.1]) == 1
+    assert _inf([0.0, 0.1], tol=0.1) == 0
+    assert _inf([0.0, 0.1], tol=0.099) == 1
+    assert _inf([1, 0], has=[1, 0]) == -2  # IncompleteGroup
+
+
+# ---- test_mockllm.cpp:24-28, 57-63 ----------------------------------------------
+def test_fnv_and_token_logprob_kats():
+    for s, want in [(b"", 14695981039346656037), (b"a", 0xAF63DC4C8601EC8C), (b"foobar", 0x85944171F73967E8)]:
+        buf = np.frombuffer(s, np.uint8) if s else np.zeros(1, np.uint8)
+        assert L.oracle_fnv1a64(buf.ctypes.data, len(s), 14695981039346656037) == want
+    for t, lp in [(0, -1.0), (3, -1.3), (6, -1.6), (7, -1.0), (10, -1.3)]:
+        assert L.oracle_token_logprob(t) == lp
+
+
+# ---- golden vectors produced by the compiled reference --------------------------
+def test_golden_flatten():
+    for c in GOLD["flatten"]:
+        ids = np.array(c["ids"] or [0], np.int64)
+        r = np.array(c["roles"] or [0], np.int32)
+        l = np.array(c["lens"] or [0], np.int64)
+        out = np.zeros(max(len(c["ids"]), 1), np.int64)
+        n = L.oracle_flatten(len(c["roles"]), r.ctypes.data, l.ctypes.data, ids.ctypes.data, c["begin"], c["end"],
+                             out.ctypes.data, len(out))
+        assert out[:n].tolist() == c["flatten_range"]
+        # the packer's token stream of a one-trajectory batch == reference flatten()
+        if c["roles"]:
+            lp = np.where(np.repeat(np.array(c["roles"]) == 2, c["lens"]), -1.0, 0.0)
+            st, pk = O.pack(_turns(c["roles"], c["lens"]), np.array(c["ids"], np.int64), lp, 1, 50001)
+            assert st == 0
+            assert pk["tokens"].tolist() == c["flatten"]
+
+
+def test_golden_validate():
+    for c in GOLD["validate"]:
+        assert L.oracle_validate_turn(c["role"], c["n_input"], c["n_output"], c["n_logprobs"]) == c["malformed"]
+
+
+def test_golden_informative():
+    for c in GOLD["informative"]:
+        n = len(c["rewards"])
+        h, f, w = (np.array(c[k], dt) for k, dt in (("has", np.int32), ("failed", np.int32), ("rewards", np.float64)))
+        ub = np.zeros(n)
+        m = L.oracle_usable_rewards(n, h.ctypes.data, f.ctypes.data, w.ctypes.data, ub.ctypes.data)
+        assert ub[:m].tolist() == c["usable"]
+        assert L.oracle_is_informative(n, h.ctypes.data, f.ctypes.data, w.ctypes.data, c["tol"]) == c["informative"]
+
+
+def test_golden_policy_generators():
+    for c in GOLD["fnv1a64"]:
+        b = c["s"].encode()
+        buf = np.frombuffer(b, np.uint8) if b else np.zeros(1, np.uint8)
+        assert L.oracle_fnv1a64(buf.ctypes.data, len(b), 14695981039346656037) == int(c["fnv1a64"])
+    for c in GOLD["hash_token"]:
+        p = np.array(c["prompt"] or [0], np.int64)
+        assert L.oracle_hash_token(int(c["seed"]), p.ctypes.data, len(c["prompt"]), c["k"], c["vocab"]) == c["token"]
+    for c in GOLD["token_logprob"]:
+        assert L.oracle_token_logprob(c["t"]) == c["lp"]
+
+
+def test_golden_hash_token_vectorised_synth():
+    """The product's synthetic id generator (synth.hash_tokens) == reference hash_token."""
+    from paper_2603_18815_b200 import synth
+    for c in GOLD["hash_token"]:
+        got = synth.hash_tokens(int(c["seed"]), c["prompt"], np.array([c["k"]], np.uint64), c["vocab"])
+        assert int(got[0]) == c["token"]
+
+
+def test_golden_workload_rewards_product():
+    """prorl_synth_rewards (product host code) == reference generate_workload."""
+    from paper_2603_18815_b200.hotpath import synth_rewards
+    for c in GOLD["workload"]:
+        got = synth_rewards(c["num_prompts"], c["n"], c["seed"], 0.5).reshape(-1)
+        assert got.tolist() == c["rewards"]
+
+
+def test_oracle_against_live_reference_when_present():
+    R = O.ref_lib()
+    if R is None:
+        pytest.skip("oracle/_ref not built (no /root/reference)")
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        n = int(rng.integers(1, 9))
+        has = (rng.random(n) > 0.1).astype(np.int32)
+        failed = (rng.random(n) < 0.25).astype(np.int32)
+        w = rng.choice([0.0, 1.0, 0.3], n)
+        tol = float(rng.choice([0.0, 0.2]))
+        args = (n, has.ctypes.data, failed.ctypes.data, w.ctypes.data, tol)
+        assert L.oracle_is_informative(*args) == R.ref_is_informative(*args)
