@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from ._native import check, ptr
+from ._native import RolloutError, check, ptr  # noqa: F401  (RolloutError re-exported)
 
 _DT = {torch.bfloat16: N.PRORL_BF16, torch.float32: N.PRORL_FP32}
 
