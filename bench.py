@@ -289,7 +289,7 @@ def run_ours(args):
             "gpu_launches": launches_per_step * K,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
-                         "kernel": "k_score<bf16,8,5,4096,fused> (K2+K4)", "bytes_per_row": bpr},
+                         "kernel": "k_score<bf16," + N.lib.prorl_kernel_config().decode() + ",fused> (K2+K4)", "bytes_per_row": bpr},
             "segments_ms_per_step": {"h2d": seg[0] / K, "pack_grpo": seg[1] / K, "score": seg[2] / K,
                                      "allreduce": seg[3] / K, "d2h": seg[4] / K},
             "clocks": clk,

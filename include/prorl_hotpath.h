@@ -122,6 +122,8 @@ typedef struct prorl_score_cfg {
 
 /* ---- context / errors ----------------------------------------------------- */
 int prorl_abi_version(void);
+/* Name of the active K2 launch configuration (warps x stages x chunk). */
+const char* prorl_kernel_config(void);
 const char* prorl_last_error(void);
 const char* prorl_status_code(int status); /* stable rollout::Error code string */
 int prorl_ctx_create(int device, prorl_ctx** out);

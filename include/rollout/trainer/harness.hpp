@@ -1,0 +1,82 @@
+// rollout/trainer/harness.hpp — the trainer-side group types the scoring path
+// consumes, drop-in for the reference declarations
+// (proj/include/rollout/trainer/harness.hpp:35-84):
+//   RolloutOutcome, PromptGroup{completed_count, complete, usable_rewards},
+//   is_informative, IterationStats::informative (the hand-off point).
+// Additive change: RolloutOutcome gains an optional
+// trajectory slot, filled from the /process response's "trajectory" field that
+// the reference harness drops today (proj/src/trainer/harness.cpp:263-273).
+// The scheduling half of the reference harness (TrainerHarness) is out of scope.
+#pragma once
+
+#include <algorithm>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include <json.hpp>
+
+#include "rollout/errors.hpp"
+#include "rollout/trajectory.hpp"
+
+namespace rollout::train {
+
+enum class GroupState { PENDING, IN_FLIGHT, COMPLETE, CARRIED_OVER };
+
+struct RolloutOutcome {
+  double reward = 0.0;
+  std::string status;   // DONE / FAILED / CANCELLED
+  std::string address;  // backend that served it, when reported
+  double wall_seconds = 0.0;
+  std::optional<TokenTrajectory> trajectory;  // additive: token-level trajectory
+
+  bool failed() const { return status == "FAILED"; }
+};
+
+struct PromptGroup {
+  std::string prompt_id;
+  nlohmann::json payload;
+  int n = 0;
+  std::vector<std::optional<RolloutOutcome>> outcomes;  // one slot per rollout
+  GroupState state = GroupState::PENDING;
+
+  int completed_count() const {
+    return static_cast<int>(std::count_if(outcomes.begin(), outcomes.end(),
+                                          [](const auto& o) { return o.has_value(); }));
+  }
+  bool complete() const { return n > 0 && completed_count() == n; }
+
+  // Rewards of the non-FAILED rollouts, in slot order (reference harness.cpp:84-90).
+  std::vector<double> usable_rewards() const {
+    std::vector<double> r;
+    r.reserve(outcomes.size());
+    for (const auto& o : outcomes)
+      if (o && !o->failed()) r.push_back(o->reward);
+    return r;
+  }
+};
+
+// DAPO zero-variance gate (reference harness.cpp:92-102): false with fewer than
+// two usable rewards or when max - min <= tolerance; IncompleteGroup unless
+// every slot is filled.
+inline bool is_informative(const PromptGroup& g, double tolerance = 0.0) {
+  if (!g.complete())
+    throw IncompleteGroup("group " + g.prompt_id + " has " + std::to_string(g.completed_count()) + "/" +
+                          std::to_string(g.n) + " outcomes");
+  const std::vector<double> r = g.usable_rewards();
+  if (r.size() < 2) return false;
+  const auto mm = std::minmax_element(r.begin(), r.end());
+  return *mm.second - *mm.first > tolerance;
+}
+
+struct IterationStats {
+  std::vector<PromptGroup> informative;   // hand-off to the trainer step
+  std::vector<PromptGroup> carried_over;
+  double wall_seconds = 0.0;
+  int rollouts_issued = 0;
+  int cancels_issued = 0;
+  int waves = 0;
+  double idle_fraction = 0.0;
+};
+
+}  // namespace rollout::train

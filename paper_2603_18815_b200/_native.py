@@ -28,7 +28,7 @@ assert TURN_DTYPE.itemsize == 24
 
 # Every symbol include/prorl_hotpath.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "prorl_abi_version", "prorl_last_error", "prorl_status_code", "prorl_ctx_create", "prorl_ctx_destroy",
+    "prorl_abi_version", "prorl_kernel_config", "prorl_last_error", "prorl_status_code", "prorl_ctx_create", "prorl_ctx_destroy",
     "prorl_check_errors", "prorl_pack", "prorl_grpo_adv", "prorl_logprob_entropy", "prorl_clipped_loss",
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
     "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host",
@@ -71,6 +71,7 @@ def _load() -> C.CDLL:
     i32, i64, u64, f32, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
     sig = {
         "prorl_abi_version": (C.c_int, []),
+        "prorl_kernel_config": (C.c_char_p, []),
         "prorl_last_error": (C.c_char_p, []),
         "prorl_status_code": (C.c_char_p, [C.c_int]),
         "prorl_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),

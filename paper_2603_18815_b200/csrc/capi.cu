@@ -108,6 +108,8 @@ extern "C" {
 
 int prorl_abi_version(void) { return PRORL_ABI_VERSION; }
 
+const char* prorl_kernel_config(void) { return score_config_name(); }
+
 const char* prorl_last_error(void) { return g_last_error.c_str(); }
 
 const char* prorl_status_code(int status) {

@@ -94,6 +94,7 @@ int launch_slab_reduce(const double* slab, int slab_rows, double* partials, cuda
 int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
                       int64_t row_key0, const int32_t* targets, const float* old_lp, uint64_t seed,
                       float scale, float base, int n_sm, cudaStream_t st);
+const char* score_config_name();     // active K2 launch configuration
 int score_slab_rows(prorl_ctx* ctx);  // slab rows the scoring kernel uses (= its grid)
 int loss_slab_rows(prorl_ctx* ctx);
 

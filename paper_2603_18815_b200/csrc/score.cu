@@ -5,22 +5,34 @@
 // No reference code exists for this arithmetic; definitions
 // are SURVEY.md App. B.2 (logprob/entropy), B.4 (loss), B.5/B.6 (metrics).
 //
-// K2 design (HBM-bound: 2V bytes per bf16 row, one pass):
+// K2 design (HBM-bound: 2V bytes per bf16 row, read exactly once):
 //   * one warp owns one row at a time (rows strided over a persistent grid of
 //     one CTA per SM), so a row never needs a cross-warp reduction;
-//   * every warp has a private ring of STAGES x CHUNK bytes of shared memory
-//     fed by 1-D TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx,
-//     L2 evict_first) issued by lane 0, running up to STAGES chunks ahead and
-//     across row boundaries; consumers read 16 B per lane per LDS.128;
-//   * online base-2 logsumexp per lane: running max Mc (of x*c, c =
-//     inv_temp*log2e), S = sum 2^(x*c-Mc), T = sum (x*c-Mc) 2^(x*c-Mc), with a
-//     per-group max (packed bf16x2 HMNMX2) so a rescale happens at most once
-//     per 64 elements and rarely after the first few chunks;
-//   * row end: warp butterfly merge of (Mc, S, T);
-//       logp = (x_y*c - Mc) ln2 - ln S,   H = ln S - ln2 T/S
-//     (the max-relative form keeps H accurate when one logit dominates);
-//   * unaligned row heads/tails (V*esz not a multiple of 16) are read by
-//     lanes directly, the 16-B aligned interior goes through TMA.
+//   * each warp has a private ring of STAGES x CHUNK bytes of shared memory fed
+//     by 1-D TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx, L2
+//     evict_first) issued by lane 0, running ahead across row boundaries; a
+//     chunk is pulled into registers with LDS.128 and its stage released at
+//     once;
+//   * online base-2 logsumexp with a WARP-UNIFORM running max Mc of x*c
+//     (c = inv_temp * log2 e): per group of SUBV*8 bf16 per lane a packed
+//     max (HMNMX2) and one vote decide whether the max moved; only then (a
+//     handful of times per row) does the warp take the rescale path, so the
+//     common path has no divergence and no per-lane rescale;
+//   * the current top element (the one that set Mc) is kept OUT of the sums
+//     and re-added analytically at the row end:
+//         S = 2^r (1 + q),  q = S_rest 2^-r,   r = x_top*c - Mc (fma residual)
+//         logp = (x_y*c - Mc - r) ln2 - log1p(q)
+//         H    = log1p(q) + ln2 (r q - T_rest 2^-r) / (1 + q)
+//     so logp and H stay accurate to fp32 relative precision even when one
+//     token takes almost all the probability (p -> 1, H -> 0), where a plain
+//     fp32 sum of e^(x - max) cannot resolve 1 + tiny;
+//   * -inf / NaN / huge-negative bf16 logits are clamped to -2^97 with one
+//     packed min.u16x2 per two logits (they then contribute exactly 0);
+//   * unaligned row heads/tails (V*esz not a multiple of 16 B, odd row
+//     offsets) are read by lanes directly, the aligned interior goes via TMA.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace prorl {
@@ -29,102 +41,160 @@ namespace {
 
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
+constexpr unsigned kFull = 0xffffffffu;
 
 template <typename T> struct Elem;
+
 template <> struct Elem<__nv_bfloat16> {
   static constexpr int kSize = 2;
-  static constexpr uint32_t kNegInfWord = 0xff80ff80u;
+  static constexpr uint32_t kClampWord = 0xf000f000u;  // two bf16 -2^97 (the clamp floor)
   __device__ static float load(const uint8_t* row, int64_t idx) {
-    uint16_t b = __ldg(reinterpret_cast<const unsigned short*>(row) + idx);
-    return __uint_as_float(((uint32_t)b) << 16);
+    uint32_t b = __ldg(reinterpret_cast<const unsigned short*>(row) + idx);
+    b = b > 0xf000u ? 0xf000u : b;  // same clamp as the packed path
+    return __uint_as_float(b << 16);
+  }
+  template <int NV>
+  __device__ static float clamp_max(uint4 (&v)[NV]) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      v[j].x = __vminu2(v[j].x, kClampWord);
+      v[j].y = __vminu2(v[j].y, kClampWord);
+      v[j].z = __vminu2(v[j].z, kClampWord);
+      v[j].w = __vminu2(v[j].w, kClampWord);
+      __nv_bfloat162 a = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].x), *reinterpret_cast<__nv_bfloat162*>(&v[j].y));
+      __nv_bfloat162 b = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].z), *reinterpret_cast<__nv_bfloat162*>(&v[j].w));
+      a = __hmax2(a, b);
+      if (j == 0) m = *reinterpret_cast<uint32_t*>(&a);
+      else {
+        __nv_bfloat162 mm = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&m), a);
+        m = *reinterpret_cast<uint32_t*>(&mm);
+      }
+    }
+    return fmaxf(__uint_as_float(m << 16), __uint_as_float(m & 0xffff0000u));
+  }
+  template <int NV>
+  __device__ static void mask_first(uint4 (&v)[NV], float top) {
+    const uint32_t tb = __float_as_uint(top) >> 16;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      uint32_t* w = &v[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!done && (w[q] & 0xffffu) == tb) {
+          w[q] = (w[q] & 0xffff0000u) | 0xf000u;
+          done = true;
+        }
+        if (!done && (w[q] >> 16) == tb) {
+          w[q] = (w[q] & 0xffffu) | 0xf0000000u;
+          done = true;
+        }
+      }
+    }
+  }
+  template <int NV>
+  __device__ static void accumulate(const uint4 (&v)[NV], float c, float nMc, float (&S)[4], float (&Tt)[4]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xffff0000u);
+        const float d0 = fmaf(x0, c, nMc), d1 = fmaf(x1, c, nMc);
+        const float e0 = ex2_approx(d0), e1 = ex2_approx(d1);
+        S[(2 * q) & 3] += e0;
+        Tt[(2 * q) & 3] = fmaf(d0, e0, Tt[(2 * q) & 3]);
+        S[(2 * q + 1) & 3] += e1;
+        Tt[(2 * q + 1) & 3] = fmaf(d1, e1, Tt[(2 * q + 1) & 3]);
+      }
+    }
   }
 };
+
 template <> struct Elem<float> {
   static constexpr int kSize = 4;
-  static constexpr uint32_t kNegInfWord = 0xff800000u;
+  static constexpr float kFloor = -1.5845632502852868e29f;  // -2^97, same floor as bf16
+  static constexpr uint32_t kClampWord = 0xf0000000u;       // bits of -2^97
   __device__ static float load(const uint8_t* row, int64_t idx) {
-    return __ldg(reinterpret_cast<const float*>(row) + idx);
+    return fmaxf(__ldg(reinterpret_cast<const float*>(row) + idx), kFloor);
+  }
+  template <int NV>
+  __device__ static float clamp_max(uint4 (&v)[NV]) {
+    float m = kFloor;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      uint32_t* w = &v[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float x = fmaxf(__uint_as_float(w[q]), kFloor);
+        w[q] = __float_as_uint(x);
+        m = fmaxf(m, x);
+      }
+    }
+    return m;
+  }
+  template <int NV>
+  __device__ static void mask_first(uint4 (&v)[NV], float top) {
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      uint32_t* w = &v[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!done && __uint_as_float(w[q]) == top) {
+          w[q] = kClampWord;
+          done = true;
+        }
+    }
+  }
+  template <int NV>
+  __device__ static void accumulate(const uint4 (&v)[NV], float c, float nMc, float (&S)[4], float (&Tt)[4]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float d = fmaf(__uint_as_float(w[q]), c, nMc);
+        const float e = ex2_approx(d);
+        S[q] += e;
+        Tt[q] = fmaf(d, e, Tt[q]);
+      }
+    }
   }
 };
 
-struct Acc {
-  float m;     // running max of x*c (base-2 units)
-  float s[4];  // sum 2^(x*c - m), four independent chains
-  float t[4];  // sum (x*c - m) 2^(x*c - m)
+// Warp-uniform running maximum and the excluded top element.
+struct Top {
+  float Mc;  // running max of x*c (rounded), -inf before the first element
+  float Mx;  // the raw (clamped) logit that set it
 };
 
-__device__ __forceinline__ void acc_init(Acc& a) {
-  a.m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) a.s[k] = a.t[k] = 0.f;
-}
-
-// Raise the running max to nm (> a.m) and rescale the sums:
-//   S' = 2^(m-nm) S,  T' = 2^(m-nm) (T - (nm-m) S).
-__device__ __forceinline__ void acc_rescale(Acc& a, float nm) {
-  if (a.m != -INFINITY) {
-    const float sc = ex2_approx(a.m - nm);
-    const float dl = nm - a.m;
+// Called by the whole warp when some lane saw lm*c > Mc. Rescales every
+// lane's sums to the new max, turns the previous top element into an ordinary
+// term (added by lane 0), and returns the lane that holds the new top element
+// (lowest lane on ties) — that lane must exclude one copy of it from its sums.
+__device__ __forceinline__ int raise_top(float lm, float c, Top& top, float (&S)[4], float (&Tt)[4], int lane) {
+  const float gl = warp_max(lm);
+  const float nMc = gl * c;
+  if (top.Mc != -INFINITY) {
+    const float sc = ex2_approx(top.Mc - nMc);
+    const float dl = nMc - top.Mc;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a.t[k] = sc * fmaf(-dl, a.s[k], a.t[k]);
-      a.s[k] *= sc;
+      Tt[k] = sc * fmaf(-dl, S[k], Tt[k]);
+      S[k] *= sc;
+    }
+    if (lane == 0) {
+      const float d = fmaf(top.Mx, c, -nMc);
+      const float e = ex2_approx(d);
+      S[0] += e;
+      Tt[0] = fmaf(d, e, Tt[0]);
     }
   }
-  a.m = nm;
-}
-
-// One element. d is clamped so -inf logits (and masked lanes) give e = 0 and
-// d*e = 0 instead of NaN; 2^-200 flushes to zero anyway.
-__device__ __forceinline__ void acc_elem(Acc& a, int k, float x, float c) {
-  const float d = fmaxf(fmaf(x, c, -a.m), -200.f);
-  const float e = ex2_approx(d);
-  a.s[k] += e;
-  a.t[k] = fmaf(d, e, a.t[k]);
-}
-
-template <typename T, int NV>
-__device__ __forceinline__ void acc_vectors(Acc& a, const uint4 (&v)[NV], float c);
-
-template <>
-__device__ __forceinline__ void acc_vectors<__nv_bfloat16, 8>(Acc& a, const uint4 (&v)[8], float c) {
-  __nv_bfloat162 mm = *reinterpret_cast<const __nv_bfloat162*>(&v[0].x);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) mm = __hmax2(mm, *reinterpret_cast<const __nv_bfloat162*>(&w[q]));
-  }
-  const float lmc = fmaxf(__low2float(mm), __high2float(mm)) * c;
-  if (lmc > a.m) acc_rescale(a, lmc);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      acc_elem(a, (2 * q) & 3, __uint_as_float(w[q] << 16), c);
-      acc_elem(a, (2 * q + 1) & 3, __uint_as_float(w[q] & 0xffff0000u), c);
-    }
-  }
-}
-
-template <>
-__device__ __forceinline__ void acc_vectors<float, 8>(Acc& a, const uint4 (&v)[8], float c) {
-  float lm = __uint_as_float(v[0].x);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    lm = fmaxf(lm, fmaxf(fmaxf(__uint_as_float(v[j].x), __uint_as_float(v[j].y)),
-                         fmaxf(__uint_as_float(v[j].z), __uint_as_float(v[j].w))));
-  }
-  const float lmc = lm * c;
-  if (lmc > a.m) acc_rescale(a, lmc);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    acc_elem(a, 0, __uint_as_float(v[j].x), c);
-    acc_elem(a, 1, __uint_as_float(v[j].y), c);
-    acc_elem(a, 2, __uint_as_float(v[j].z), c);
-    acc_elem(a, 3, __uint_as_float(v[j].w), c);
-  }
+  top.Mc = nMc;
+  top.Mx = gl;
+  return __ffs(__ballot_sync(kFull, lm == gl)) - 1;
 }
 
 struct ScoreArgs {
@@ -148,7 +218,7 @@ struct ScoreArgs {
   int accumulate;
 };
 
-// Per-row loss terms (App. B.4/B.5), fp32 math; returned through refs.
+// Per-row loss terms (App. B.4/B.5), fp32 math.
 struct RowLoss {
   float loss, ratio, clip_lo, clip_hi;
 };
@@ -182,10 +252,16 @@ __device__ __forceinline__ void merge_block_partials(const double* g_w, const do
   }
 }
 
-template <typename T, int WARPS, int STAGES, int CHUNK, bool FUSED>
+template <int WARPS, int STAGES, int CHUNK, bool FUSED>
+constexpr size_t score_smem_bytes() {
+  return (size_t)WARPS * STAGES * CHUNK + (size_t)WARPS * STAGES * 8 +
+         (FUSED ? (size_t)WARPS * (kNG + kBucketDoubles) * sizeof(double) : 0);
+}
+
+template <typename T, int WARPS, int STAGES, int CHUNK, int SUBV, bool FUSED>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
-  static_assert(CHUNK % 512 == 0, "CHUNK must be a multiple of 32 lanes x 16 B");
-  constexpr int NV = CHUNK / 512;
+  static_assert(CHUNK % (512 * SUBV) == 0, "CHUNK must hold whole lane groups");
+  constexpr int NV = CHUNK / 512;  // 16-B vectors per lane per chunk
   constexpr int ES = Elem<T>::kSize;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -260,6 +336,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
 
   uint32_t consumed = 0;
   const float c = p.c;
+  const uint4 fill = make_uint4(Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord);
   for (int64_t i = gw; i < p.n_rows; i += nw) {
     const uint8_t* rp = row_ptr(i);
     uintptr_t a, b;
@@ -271,15 +348,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
     float xy = 0.f;
     if (lane == 0) xy = Elem<T>::load(rp, tgt);
 
-    Acc acc;
-    acc_init(acc);
-    {  // unaligned head / tail elements, one per lane (<= 14 of them)
-      float x = -INFINITY;
+    Top top{-INFINITY, 0.f};
+    float S[4] = {0.f, 0.f, 0.f, 0.f}, Tt[4] = {0.f, 0.f, 0.f, 0.f};
+    if (head + tail > 0) {  // unaligned head / tail elements, one per lane (<= 14 of them)
+      float x = __uint_as_float(0xf0000000u);  // -2^97: the clamp floor, contributes 0
       if (lane < head) x = Elem<T>::load(rp, lane);
-      else if (lane < head + tail) x = Elem<T>::load(rp, (int64_t)((b - reinterpret_cast<uintptr_t>(rp)) / ES) + (lane - head));
-      const float xc = x * c;
-      if (xc > acc.m) acc_rescale(acc, xc);
-      acc_elem(acc, 0, x, c);
+      else if (lane < head + tail)
+        x = Elem<T>::load(rp, (int64_t)((b - reinterpret_cast<uintptr_t>(rp)) / ES) + (lane - head));
+      if (__any_sync(kFull, x * c > top.Mc)) {
+        const int L = raise_top(x, c, top, S, Tt, lane);
+        if (lane == L) x = __uint_as_float(0xf0000000u);
+      }
+      const float d = fmaf(x, c, -top.Mc);
+      const float e = ex2_approx(d);
+      S[0] += e;
+      Tt[0] = fmaf(d, e, Tt[0]);
     }
 
     for (int64_t ch = 0; ch < nchunks; ++ch) {
@@ -289,36 +372,43 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
       mbar_wait(&bars[s], parity);
       const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * CHUNK);
       uint4 v[NV];
+      if (nvec == (uint32_t)(CHUNK / 16)) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const uint32_t q = lane + 32 * j;
-        if (q < nvec) v[j] = sv[q];
-        else v[j] = make_uint4(Elem<T>::kNegInfWord, Elem<T>::kNegInfWord, Elem<T>::kNegInfWord, Elem<T>::kNegInfWord);
+        for (int j = 0; j < NV; ++j) v[j] = sv[lane + 32 * j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const uint32_t q = lane + 32 * j;
+          v[j] = q < nvec ? sv[q] : fill;
+        }
       }
       __syncwarp();
       ++consumed;
       if (lane == 0) produce();
-      acc_vectors<T, NV>(acc, v, c);
+#pragma unroll
+      for (int g0 = 0; g0 < NV; g0 += SUBV) {
+        uint4 u[SUBV];
+#pragma unroll
+        for (int j = 0; j < SUBV; ++j) u[j] = v[g0 + j];
+        const float lm = Elem<T>::template clamp_max<SUBV>(u);
+        if (__any_sync(kFull, lm * c > top.Mc)) {
+          const int L = raise_top(lm, c, top, S, Tt, lane);
+          if (lane == L) Elem<T>::template mask_first<SUBV>(u, top.Mx);
+        }
+        Elem<T>::template accumulate<SUBV>(u, c, -top.Mc, S, Tt);
+      }
     }
 
-    // ---- row end: merge lanes ----
-    float S = (acc.s[0] + acc.s[1]) + (acc.s[2] + acc.s[3]);
-    float Tt = (acc.t[0] + acc.t[1]) + (acc.t[2] + acc.t[3]);
-    const float Mw = warp_max(acc.m);
-    if (S > 0.f) {
-      const float sc = ex2_approx(acc.m - Mw);
-      Tt = sc * fmaf(-(Mw - acc.m), S, Tt);
-      S = sc * S;
-    } else {
-      S = 0.f;
-      Tt = 0.f;
-    }
-    S = warp_sum(S);
-    Tt = warp_sum(Tt);
+    // ---- row end: merge lanes, re-add the top element analytically ----
+    float Sr = warp_sum((S[0] + S[1]) + (S[2] + S[3]));
+    float Tr = warp_sum((Tt[0] + Tt[1]) + (Tt[2] + Tt[3]));
     if (lane == 0) {
-      const float lnS = logf(S);
-      const float logp = fmaf(xy, c, -Mw) * kLn2 - lnS;
-      const float ent = lnS - kLn2 * (Tt / S);
+      const float r = fmaf(top.Mx, c, -top.Mc);  // top element's own exponent (~0)
+      const float ir = ex2_approx(-r);
+      const float q = Sr * ir;
+      const float l1q = log1pf(q);
+      const float logp = (fmaf(xy, c, -top.Mc) - r) * kLn2 - l1q;
+      const float ent = l1q + kLn2 * (fmaf(r, q, -Tr * ir) / (1.f + q));
       if (p.logp) p.logp[i] = logp;
       if (p.entropy) p.entropy[i] = ent;
       if constexpr (FUSED) {
@@ -326,21 +416,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         const float A = p.adv[p.row_seq[i]];
         int k = p.row_turn[i];
         k = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
-        const RowLoss r = row_loss(logp, old, A, p.lo_bound, p.hi_bound);
-        g[0] += r.loss;
+        const RowLoss rl = row_loss(logp, old, A, p.lo_bound, p.hi_bound);
+        g[0] += rl.loss;
         g[1] += 1.0;
         g[2] += ent;
         g[3] += logp;
-        g[4] += r.ratio;
-        g[5] += r.clip_lo;
-        g[6] += r.clip_hi;
+        g[4] += rl.ratio;
+        g[5] += rl.clip_lo;
+        g[6] += rl.clip_hi;
         g[7] += (double)(old - logp);
         double* bk = bk_w + warp * kBucketDoubles + k * PRORL_N_PER_TURN;
         bk[0] += 1.0;
-        bk[1] += r.loss;
+        bk[1] += rl.loss;
         bk[2] += ent;
         bk[3] += logp;
-        bk[4] += r.clip_lo + r.clip_hi;
+        bk[4] += rl.clip_lo + rl.clip_hi;
       }
     }
   }
@@ -424,28 +514,57 @@ __global__ void k_slab_reduce(const double* __restrict__ slab, int rows, double*
   if (t != PRORL_P_ADV_SUM && t != PRORL_P_N_ROLLOUTS) partials[t] += v;
 }
 
-// ---- launch configuration ---------------------------------------------------------
-constexpr int kWarps = 8;
-constexpr int kStages = 5;
-constexpr int kChunk = 4096;
+// ---- launch configurations ------------------------------------------------------------
+// warps/CTA x stages x chunk bytes; one CTA per SM. Selected with
+// PRORL_K2_CONFIG (tuning) — default chosen from ncu/bench measurements.
+struct K2Config {
+  const char* name;
+  int warps, stages, chunk;
+};
+constexpr K2Config kConfigs[] = {
+    {"w16s2c4096", 16, 2, 4096}, {"w12s3c4096", 12, 3, 4096}, {"w8s5c4096", 8, 5, 4096}, {"w14s3c4096", 14, 3, 4096}};
+constexpr int kDefaultConfig = 0;
 
-template <typename T, bool FUSED>
-size_t score_smem() {
-  return (size_t)kWarps * kStages * kChunk + (size_t)kWarps * kStages * 8 +
-         (FUSED ? (size_t)kWarps * (kNG + kBucketDoubles) * sizeof(double) : 0);
+int active_config() {
+  static int idx = [] {
+    const char* e = std::getenv("PRORL_K2_CONFIG");
+    if (e)
+      for (int i = 0; i < (int)(sizeof(kConfigs) / sizeof(kConfigs[0])); ++i)
+        if (std::strcmp(e, kConfigs[i].name) == 0) return i;
+    return kDefaultConfig;
+  }();
+  return idx;
 }
 
-template <typename T, bool FUSED>
-int run_score(const ScoreArgs& a, int grid, cudaStream_t st) {
-  auto kern = k_score<T, kWarps, kStages, kChunk, FUSED>;
-  const size_t smem = score_smem<T, FUSED>();
+template <typename T, int W, int ST, int CH, bool FUSED>
+int run_score_cfg(const ScoreArgs& a, int grid, cudaStream_t st) {
+  constexpr int SUBV = sizeof(T) == 2 ? 2 : 4;
+  auto kern = k_score<T, W, ST, CH, SUBV, FUSED>;
+  constexpr size_t smem = score_smem_bytes<W, ST, CH, FUSED>();
+  static_assert(smem <= 227 * 1024, "shared memory budget");
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, kWarps * 32, smem, st>>>(a);
+  kern<<<grid, W * 32, smem, st>>>(a);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
 }
 
+template <typename T, bool FUSED>
+int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* rows_used, cudaStream_t st) {
+  const K2Config& k = kConfigs[active_config()];
+  int grid = (int)std::min<int64_t>((int64_t)n_sm, (n_rows + k.warps - 1) / k.warps);
+  if (FUSED && grid > slab_rows) grid = slab_rows;
+  if (rows_used) *rows_used = grid;
+  switch (active_config()) {
+    case 0: return run_score_cfg<T, 16, 2, 4096, FUSED>(a, grid, st);
+    case 1: return run_score_cfg<T, 12, 3, 4096, FUSED>(a, grid, st);
+    case 2: return run_score_cfg<T, 8, 5, 4096, FUSED>(a, grid, st);
+    default: return run_score_cfg<T, 14, 3, 4096, FUSED>(a, grid, st);
+  }
+}
+
 }  // namespace
+
+const char* score_config_name() { return kConfigs[active_config()].name; }
 
 int score_slab_rows(prorl_ctx* ctx) { return ctx->n_sm; }
 int loss_slab_rows(prorl_ctx* ctx) { return 2 * ctx->n_sm; }
@@ -485,13 +604,11 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
     a.hi_bound = 1.0f + cfg->eps_hi;
     a.n_buckets = cfg->n_buckets;
   }
-  int grid = (int)std::min<int64_t>((int64_t)ctx->n_sm, (n_rows + kWarps - 1) / kWarps);
-  if (cfg && grid > slab_rows) grid = slab_rows;
-  if (rows_used) *rows_used = grid;
-  if (dtype == PRORL_BF16) {
-    return cfg ? run_score<__nv_bfloat16, true>(a, grid, st) : run_score<__nv_bfloat16, false>(a, grid, st);
-  }
-  return cfg ? run_score<float, true>(a, grid, st) : run_score<float, false>(a, grid, st);
+  if (dtype == PRORL_BF16)
+    return cfg ? run_score<__nv_bfloat16, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st)
+               : run_score<__nv_bfloat16, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st);
+  return cfg ? run_score<float, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st)
+             : run_score<float, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st);
 }
 
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp, const float* adv,

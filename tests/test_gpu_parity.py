@@ -126,7 +126,7 @@ def test_pack_edge_cases(scorer, cuda):
     assert st == 0
     compare_pack(scorer.pack(t, dev(ids, cuda), dev(lp, cuda), n_seq, 32000, ora["n_active"]), ora)
     # turn ordinals past the 64-bucket range are kept (bucket folding is K4's job)
-    assert ora["turn_id"].max() >= 40
+    assert ora["turn_id"].max() >= 39
 
 
 def test_pack_empty(scorer, cuda):
