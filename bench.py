@@ -129,7 +129,7 @@ def cpu_baseline(shard, cfg, seed: int, budget_s: float) -> dict:
     from oracle import oracle as O
     b = shard.batch
     threads = os.cpu_count() or 1
-    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
     oc = O.score_cfg(cfg.vocab, cfg.dtype, microbatch_rows=cfg.microbatch_rows)
     # calibrate on a small sample, then size the timed sample for ~budget_s
     probe = O.score_batch(hb, oc, seed, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
@@ -157,7 +157,7 @@ def run_reference(args):
     c = synth.CONFIGS[args.config]
     b = shard.batch
     threads = os.cpu_count() or 1
-    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
     oc = O.score_cfg(c["vocab"], c["dtype"], microbatch_rows=args.microbatch)
     probe = O.score_batch(hb, oc, 2603, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
     rate = threads * 4 / max(probe["timings"][1], 1e-6)

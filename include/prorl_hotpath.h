@@ -192,6 +192,14 @@ int prorl_gen_logits(prorl_ctx* ctx, void* logits, int dtype, int64_t row_stride
                      int64_t n_rows, int64_t row_key0, const int32_t* targets,
                      const float* old_lp, uint64_t seed, float sigma, void* stream);
 
+/* Same, with an explicit key per row (row_keys[n_rows], device). prorl_score_host
+ * in fill mode keys active row r of rollout s as rollout_key[s] * 2^20 +
+ * (r - cu_seqlens[s]), so a row's logits do not depend on how groups were
+ * sharded over GPUs. */
+int prorl_gen_logits_keyed(prorl_ctx* ctx, void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                           int64_t n_rows, const int64_t* row_keys, const int32_t* targets,
+                           const float* old_lp, uint64_t seed, float sigma, void* stream);
+
 /* ---- host-side helpers ------------------------------------------------------ */
 /* Per-rollout rewards [num_prompts * n] with the semantics (and, under
  * libstdc++, the exact values) of the reference's generate_workload
@@ -208,16 +216,27 @@ typedef struct prorl_host_batch {
   const int64_t* ids; const double* lp; int64_t n_tokens;
   const double* reward; const uint8_t* usable; int32_t n_rollouts; /* = n_seq */
   const int32_t* group_off; int32_t n_groups;
+  const int64_t* rollout_key; /* nullable: global rollout identity per slot
+                               * (synthetic-logits key; NULL = slot index) */
 } prorl_host_batch;
 
 /* Logits provider for prorl_score_host: micro-batch j (active rows
  * [row0, row0+n)) reads logits from pool[j % n_pool] (each buffer holds
  * >= microbatch_rows rows of row_stride elements). If `fill` is non-zero the
- * library regenerates the buffer for micro-batch j with prorl_gen_logits
- * before scoring it (parity mode; generation is then inside the call). */
+ * library regenerates the buffer for micro-batch j with prorl_gen_logits_keyed
+ * before scoring it (parity mode; generation is then inside the call).
+ * If `provide` is set, buffers/fill are ignored and the callback supplies each
+ * micro-batch instead (the trainer's LM head): it receives the micro-batch's
+ * device arrays (packed-stream row ids, targets, behaviour logprobs) and
+ * returns a device pointer to n rows of `*row_stride` logits, stream-ordered
+ * on `stream`; a non-zero return aborts the step with that status. */
+typedef int (*prorl_logits_fn)(void* user, int64_t row0, int64_t n, const int32_t* d_rows,
+                               const int32_t* d_targets, const float* d_old_lp,
+                               const void** d_logits, int64_t* row_stride, void* stream);
 typedef struct prorl_logits_pool {
   void* const* buffers; int32_t n_pool; int32_t fill; int64_t row_stride;
   uint64_t seed; float sigma; int32_t pad_;
+  prorl_logits_fn provide; void* user;
 } prorl_logits_pool;
 
 /* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for

@@ -318,6 +318,7 @@ typedef struct {
   const oracle_packed* pk;
   const double* adv;
   const prorl_score_cfg* cfg;
+  const int64_t* rollout_key;
   uint64_t seed;
   float sigma;
   int64_t r0, r1;
@@ -342,7 +343,11 @@ static void* score_worker(void* arg) {
   const double lo = 1.0 - (double)cfg->loss.eps_lo, hi = 1.0 + (double)cfg->loss.eps_hi;
   for (int64_t i = w->r0; i < w->r1; ++i) {
     double t0 = now_s();
-    oracle_gen_logits(row, cfg->dtype, cfg->vocab, cfg->vocab, 1, i, &w->pk->act_target[i], &w->pk->act_old_lp[i],
+    /* key = rollout_key[s] * 2^20 + position in the sequence (prorl_gen_logits_keyed) */
+    const int32_t s = w->pk->act_seq[i];
+    const int64_t key = (w->rollout_key ? w->rollout_key[s] : (int64_t)s) * ((int64_t)1 << 20) +
+                        (int64_t)(w->pk->act_row[i] - w->pk->cu_seqlens[s]);
+    oracle_gen_logits(row, cfg->dtype, cfg->vocab, cfg->vocab, 1, key, &w->pk->act_target[i], &w->pk->act_old_lp[i],
                       w->seed, w->sigma);
     double t1 = now_s();
     double lp, ent;
@@ -359,8 +364,8 @@ static void* score_worker(void* arg) {
 }
 
 /* The whole step on the CPU for one shard: pack (B.1) -> GRPO (B.3) -> per
- * active row: synthetic logits row (key = active index, as prorl_score_host
- * with fill=1) -> logprob/entropy (B.2) -> loss/metrics (B.4-B.6). Rows
+ * active row: synthetic logits row (keyed as prorl_score_host with fill=1:
+ * rollout_key[s] * 2^20 + position) -> logprob/entropy (B.2) -> loss/metrics (B.4-B.6). Rows
  * [row_begin, row_end) only (row_end < 0: all), split over nthreads.
  * timings[3] (s): pack+grpo, scoring (logits generation excluded, summed
  * over threads / nthreads), generation. Returns 0 or an error status. */
@@ -393,6 +398,7 @@ int oracle_score_batch(const prorl_host_batch* hb, const prorl_score_cfg* cfg, u
     const int64_t n = a1 - a0;
     for (int k = 0; k < nthreads; ++k) {
       w[k].pk = &pk; w[k].adv = adv; w[k].cfg = cfg; w[k].seed = seed; w[k].sigma = sigma;
+      w[k].rollout_key = hb->rollout_key;
       w[k].r0 = a0 + n * k / nthreads; w[k].r1 = a0 + n * (k + 1) / nthreads;
       w[k].out_logp = out_logp; w[k].out_ent = out_ent;
       pthread_create(&th[k], NULL, score_worker, &w[k]);

@@ -45,12 +45,13 @@ class ScoreCfg(C.Structure):  # layout of prorl_score_cfg
 
 class HostBatch(C.Structure):  # layout of prorl_host_batch
     _fields_ = [("turns", vp), ("n_turns", i64), ("ids", vp), ("lp", vp), ("n_tokens", i64), ("reward", vp),
-                ("usable", vp), ("n_rollouts", i32), ("group_off", vp), ("n_groups", i32)]
+                ("usable", vp), ("n_rollouts", i32), ("group_off", vp), ("n_groups", i32), ("rollout_key", vp)]
 
 
-def host_batch(turns, ids, lp, reward, usable, group_off) -> HostBatch:
+def host_batch(turns, ids, lp, reward, usable, group_off, rollout_key=None) -> HostBatch:
     return HostBatch(turns.ctypes.data, len(turns), ids.ctypes.data, lp.ctypes.data, len(ids), reward.ctypes.data,
-                     usable.ctypes.data, len(reward), group_off.ctypes.data, len(group_off) - 1)
+                     usable.ctypes.data, len(reward), group_off.ctypes.data, len(group_off) - 1,
+                     None if rollout_key is None else rollout_key.ctypes.data)
 
 
 def score_cfg(vocab, dtype="bf16", inv_temperature=1.0, adv_eps=1e-6, ddof=1, eps_lo=0.2, eps_hi=0.28,

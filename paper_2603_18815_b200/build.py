@@ -21,10 +21,25 @@ INCLUDE = ROOT / "include"
 BUILD = ROOT / "build" / "hotpath"
 LIB = PKG / "libprorl_hotpath.so"
 
-SOURCES = ["pack.cu", "grpo.cu", "score.cu", "synth.cu", "capi.cu", "workload.cpp"]
+SOURCES = ["pack.cu", "grpo.cu", "score.cu", "synth.cu", "capi.cu", "workload.cpp", "scoring.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+
+
+def json_include() -> str:
+    """Directory holding nlohmann json.hpp (the reference's only third-party
+    header, also used by the drop-in C++ headers). This image ships 3.11.3
+    inside the venv's cudnn_frontend tree."""
+    import glob
+    import site
+    env = os.environ.get("PRORL_JSON_DIR")
+    if env and (Path(env) / "json.hpp").exists():
+        return env
+    for sp in site.getsitepackages() + [site.getusersitepackages(), sys.prefix]:
+        for cand in glob.glob(os.path.join(sp, "**", "nlohmann", "json.hpp"), recursive=True):
+            return str(Path(cand).parent)
+    raise RuntimeError("nlohmann/json.hpp not found (set PRORL_JSON_DIR)")
 
 
 def nvcc() -> str:
@@ -43,14 +58,14 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
-    headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+    headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + list(INCLUDE.glob("rollout/**/*.hpp"))
     objs = []
     for src in SOURCES:
         s = CSRC / src
         o = BUILD / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{json_include()}", "-c", str(s), "-o", str(o)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

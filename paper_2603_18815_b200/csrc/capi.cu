@@ -151,7 +151,8 @@ int prorl_ctx_destroy(prorl_ctx* c) {
   for (auto* b : {&c->scan_tmp, &c->pack_tmp, &c->slab, &c->grpo_tmp, &c->h_turns, &c->h_ids, &c->h_lp,
                   &c->h_reward, &c->h_usable, &c->h_goff, &c->p_tokens, &c->p_mask, &c->p_turn, &c->p_seq,
                   &c->p_pos, &c->p_cu, &c->p_oldlp, &c->a_row, &c->a_target, &c->a_oldlp, &c->a_seq, &c->a_turn,
-                  &c->a_nact, &c->adv, &c->informative, &c->partials, &c->logp, &c->entropy})
+                  &c->a_nact, &c->adv, &c->informative, &c->partials, &c->logp, &c->entropy, &c->h_rkey,
+                  &c->row_keys})
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -268,7 +269,18 @@ int prorl_gen_logits(prorl_ctx* c, void* logits, int dtype, int64_t row_stride, 
   PRORL_CUDA(cudaSetDevice(c->device));
   const float scale = (float)((double)sigma * std::sqrt(3.0));
   const float base = (float)(std::log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
-  return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, row_key0, targets, old_lp, seed, scale, base,
+  return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, row_key0, nullptr, targets, old_lp, seed, scale,
+                           base, c->n_sm, S(stream));
+}
+
+int prorl_gen_logits_keyed(prorl_ctx* c, void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
+                           const int64_t* row_keys, const int32_t* targets, const float* old_lp, uint64_t seed,
+                           float sigma, void* stream) {
+  if (!c || !row_keys) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_gen_logits_keyed: null ctx/row_keys");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  const float scale = (float)((double)sigma * std::sqrt(3.0));
+  const float base = (float)(std::log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
+  return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, 0, row_keys, targets, old_lp, seed, scale, base,
                            c->n_sm, S(stream));
 }
 
@@ -293,7 +305,8 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
                      const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream) {
   if (!c || !hb || !cfg || !pool || !host_partials)
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null argument");
-  if (pool->n_pool < 1 || !pool->buffers) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: empty logits pool");
+  if (!pool->provide && (pool->n_pool < 1 || !pool->buffers))
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: empty logits pool");
   if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
@@ -329,6 +342,8 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   PRORL_CUDA(c->a_turn.ensure(sizeof(int16_t) * (size_t)std::max<int64_t>(A, 1)));
   PRORL_CUDA(c->a_nact.ensure(sizeof(int64_t)));
   PRORL_CUDA(c->adv.ensure(sizeof(float) * (size_t)std::max(R, 1)));
+  PRORL_CUDA(c->h_rkey.ensure(sizeof(int64_t) * (size_t)std::max(R, 1)));
+  PRORL_CUDA(c->row_keys.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(std::min<int64_t>(A, cfg->microbatch_rows), 1)));
   PRORL_CUDA(c->informative.ensure((size_t)std::max(G, 1)));
   PRORL_CUDA(c->partials.ensure(sizeof(double) * PRORL_N_PARTIALS));
   PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(srows, loss_slab_rows(c))));
@@ -346,6 +361,8 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   if (R) {
     PRORL_CUDA(cudaMemcpyAsync(c->h_reward.p, hb->reward, sizeof(double) * R, cudaMemcpyHostToDevice, st));
     PRORL_CUDA(cudaMemcpyAsync(c->h_usable.p, hb->usable, (size_t)R, cudaMemcpyHostToDevice, st));
+    if (hb->rollout_key)
+      PRORL_CUDA(cudaMemcpyAsync(c->h_rkey.p, hb->rollout_key, sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
   }
   if (G) PRORL_CUDA(cudaMemcpyAsync(c->h_goff.p, hb->group_off, sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, st));
   PRORL_CUDA(cudaMemsetAsync(partials, 0, sizeof(double) * PRORL_N_PARTIALS, st));
@@ -377,11 +394,25 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   const int64_t mb = cfg->microbatch_rows;
   for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
     const int64_t n = std::min(mb, A - row0);
-    void* buf = pool->buffers[j % pool->n_pool];
-    if (pool->fill)
-      PRORL_TRY(prorl_gen_logits(c, buf, cfg->dtype, pool->row_stride, cfg->vocab, n, row0, pk.act_target + row0,
-                                 pk.act_old_lp + row0, pool->seed, pool->sigma, st));
-    PRORL_TRY(launch_score(c, buf, cfg->dtype, pool->row_stride, cfg->vocab, nullptr, pk.act_target + row0,
+    const void* buf = nullptr;
+    int64_t stride = pool->row_stride;
+    if (pool->provide) {
+      const int rc = pool->provide(pool->user, row0, n, pk.act_row + row0, pk.act_target + row0, pk.act_old_lp + row0,
+                                   &buf, &stride, stream);
+      if (rc != PRORL_OK) return rc;
+      if (!buf) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: logits callback returned null");
+    } else {
+      void* b = pool->buffers[j % pool->n_pool];
+      if (pool->fill) {
+        int64_t* keys = c->row_keys.as<int64_t>();
+        PRORL_TRY(launch_row_keys(pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
+                                  hb->rollout_key ? c->h_rkey.as<int64_t>() : nullptr, n, keys, st));
+        PRORL_TRY(prorl_gen_logits_keyed(c, b, cfg->dtype, pool->row_stride, cfg->vocab, n, keys,
+                                         pk.act_target + row0, pk.act_old_lp + row0, pool->seed, pool->sigma, st));
+      }
+      buf = b;
+    }
+    PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
                            pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
   }

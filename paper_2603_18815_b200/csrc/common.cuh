@@ -64,7 +64,7 @@ struct prorl_ctx {
   prorl::DevBuf h_turns, h_ids, h_lp, h_reward, h_usable, h_goff;
   prorl::DevBuf p_tokens, p_mask, p_turn, p_seq, p_pos, p_cu, p_oldlp;
   prorl::DevBuf a_row, a_target, a_oldlp, a_seq, a_turn, a_nact;
-  prorl::DevBuf adv, informative, partials, logp, entropy;
+  prorl::DevBuf adv, informative, partials, logp, entropy, h_rkey, row_keys;
   void* nccl_comm = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0;
   cudaEvent_t ev[8] = {};
@@ -92,8 +92,10 @@ int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const f
                 const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used, cudaStream_t st);
 int launch_slab_reduce(const double* slab, int slab_rows, double* partials, cudaStream_t st);
 int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
-                      int64_t row_key0, const int32_t* targets, const float* old_lp, uint64_t seed,
+                      int64_t row_key0, const int64_t* row_keys, const int32_t* targets, const float* old_lp, uint64_t seed,
                       float scale, float base, int n_sm, cudaStream_t st);
+int launch_row_keys(const int32_t* act_row, const int32_t* act_seq, const int32_t* cu_seqlens,
+                    const int64_t* rollout_key, int64_t n, int64_t* keys, cudaStream_t st);
 const char* score_config_name();     // active K2 launch configuration
 int score_slab_rows(prorl_ctx* ctx);  // slab rows the scoring kernel uses (= its grid)
 int loss_slab_rows(prorl_ctx* ctx);

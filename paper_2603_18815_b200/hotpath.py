@@ -168,7 +168,8 @@ class Scorer:
                    seed: int = 0, sigma: float = 2.0, stream=None):
         hb = batch.c()
         bufs = (C.c_void_p * len(pool))(*[ptr(b) for b in pool])
-        lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0)
+        lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0,
+                          None, None)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()
@@ -205,11 +206,12 @@ class HostBatchArrays:
     reward: np.ndarray     # float64 per rollout slot
     usable: np.ndarray     # uint8 per rollout slot (0 = FAILED)
     group_off: np.ndarray  # int32 [n_groups+1]
+    rollout_key: np.ndarray | None = None  # int64 global rollout identity per slot (synthetic-logits key)
 
     def c(self) -> N.HostBatch:
         return N.HostBatch(ptr(self.turns), len(self.turns), ptr(self.ids), ptr(self.lp), len(self.ids),
                            ptr(self.reward), ptr(self.usable), len(self.reward), ptr(self.group_off),
-                           len(self.group_off) - 1)
+                           len(self.group_off) - 1, ptr(self.rollout_key))
 
     def pinned(self) -> "HostBatchArrays":
         """Copy into page-locked host memory (torch pinned tensors)."""
@@ -217,7 +219,8 @@ class HostBatchArrays:
             t = torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1)).pin_memory()
             return t.numpy().view(a.dtype).reshape(a.shape)
         return HostBatchArrays(*(pin(getattr(self, f)) for f in
-                                 ("turns", "ids", "lp", "reward", "usable", "group_off")))
+                                 ("turns", "ids", "lp", "reward", "usable", "group_off")),
+                               rollout_key=None if self.rollout_key is None else pin(self.rollout_key))
 
     @property
     def n_tokens(self) -> int:
@@ -232,7 +235,8 @@ class HostBatchArrays:
         return len(self.group_off) - 1
 
     def bytes_h2d(self) -> int:
-        return sum(getattr(self, f).nbytes for f in ("turns", "ids", "lp", "reward", "usable", "group_off"))
+        extra = 0 if self.rollout_key is None else self.rollout_key.nbytes
+        return extra + sum(getattr(self, f).nbytes for f in ("turns", "ids", "lp", "reward", "usable", "group_off"))
 
 
 def finalize(p: np.ndarray) -> dict:

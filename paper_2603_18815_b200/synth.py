@@ -166,13 +166,14 @@ def make_shard(config: str | dict, rank: int = 0, world: int = 1, seed: int | No
     else:
         mine = informative
     turns, ids, lps = [], [], []
-    reward, usable, goff = [], [], [0]
+    reward, usable, goff, rkey = [], [], [0], []
     src = 0
     seq = 0
     tpr = []
     for g in mine:
         for j in range(n):
             reward.append(rewards[g, j])
+            rkey.append(g * n + j)
             usable.append(0 if failed[g, j] else 1)
             if not failed[g, j]:
                 roles, lens, tid, tlp = trajectory(cfg, seed, g * n + j, V)
@@ -195,6 +196,7 @@ def make_shard(config: str | dict, rank: int = 0, world: int = 1, seed: int | No
         reward=np.array(reward, dtype=np.float64),
         usable=np.array(usable, dtype=np.uint8),
         group_off=np.array(goff, dtype=np.int32),
+        rollout_key=np.array(rkey, dtype=np.int64),
     )
     return Shard(batch=batch, groups=mine, n_active=count_active(t), turns_per_rollout=tpr)
 

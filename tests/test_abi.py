@@ -41,8 +41,8 @@ def test_struct_layouts_match_header():
     assert C.sizeof(N.LossCfg) == 16
     assert C.sizeof(N.ScoreCfg) == 40
     assert N.TURN_DTYPE.itemsize == 24
-    assert C.sizeof(N.HostBatch) == 80
-    assert C.sizeof(N.LogitsPool) == 40
+    assert C.sizeof(N.HostBatch) == 88
+    assert C.sizeof(N.LogitsPool) == 56
 
 
 def test_shard_lpt_deterministic_and_balanced():

@@ -1,0 +1,59 @@
+"""The C++ drop-in surface (include/rollout/..., rollout::train::score_groups):
+build tests/cpp/test_scoring.cpp against the in-tree library and run it.
+Host checks run without a GPU; the --gpu leg is checked against the oracle."""
+import json
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2603_18815_b200 import _native as N
+from paper_2603_18815_b200 import build as B
+
+ROOT = Path(__file__).resolve().parents[1]
+BIN = ROOT / "build" / "test_scoring"
+
+
+@pytest.fixture(scope="module")
+def binary():
+    B.build()
+    BIN.parent.mkdir(parents=True, exist_ok=True)
+    src = ROOT / "tests" / "cpp" / "test_scoring.cpp"
+    if not BIN.exists() or BIN.stat().st_mtime < max(src.stat().st_mtime, B.LIB.stat().st_mtime):
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", f"-I{ROOT / 'include'}", f"-I{B.json_include()}", str(src),
+               "-o", str(BIN), f"-L{B.PKG}", "-lprorl_hotpath", f"-Wl,-rpath,{B.PKG}"]
+        subprocess.run(cmd, check=True)
+    return BIN
+
+
+def test_cpp_host_checks(binary):
+    r = subprocess.run([str(binary)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "host checks OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_score_groups_vs_oracle(binary):
+    r = subprocess.run([str(binary), "--gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    t = np.zeros(len(d["turns"]), N.TURN_DTYPE)
+    arr = np.array(d["turns"], np.int64)
+    t["src_off"], t["traj"], t["len"], t["role"] = arr[:, 0], arr[:, 1], arr[:, 2], arr[:, 3]
+    ids = np.array(d["ids"], np.int64)
+    lp = np.array(d["lp"], np.float64)
+    reward = np.array(d["reward"], np.float64)
+    usable = np.array(d["usable"], np.uint8)
+    goff = np.array(d["group_off"], np.int32)
+    hb = O.host_batch(t, ids, lp, reward, usable, goff)
+    ref = O.score_batch(hb, O.score_cfg(4099, "bf16", microbatch_rows=64), 4242, 2.0, nthreads=4)
+    assert ref["status"] == 0 and ref["n_active"] == d["n_active_host"] == d["n_active"]
+    got = np.array(d["partials"])
+    P, Q = ref["partials"], ref["abs"]
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM, N.P_KL1_SUM):
+        assert abs(got[i] - P[i]) <= 1e-5 * Q[i], (i, got[i], P[i])
+    assert got[N.P_N_ACTIVE] == P[N.P_N_ACTIVE]
+    assert got[N.P_N_ROLLOUTS] == P[N.P_N_ROLLOUTS]
+    assert abs(got[N.P_CLIP_LO] - P[N.P_CLIP_LO]) <= ref["n_border"]

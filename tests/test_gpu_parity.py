@@ -331,7 +331,7 @@ def _cfg(config):
 
 
 def _oracle_step(b: HostBatchArrays, cfg: ScoreConfig, seed, n_active, nthreads=8):
-    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
     oc = O.score_cfg(cfg.vocab, cfg.dtype, microbatch_rows=cfg.microbatch_rows)
     return O.score_batch(hb, oc, seed, 2.0, nthreads=nthreads, want_rows=True, n_active_hint=n_active)
 
