@@ -200,6 +200,11 @@ int prorl_gen_logits_keyed(prorl_ctx* ctx, void* logits, int dtype, int64_t row_
                            int64_t n_rows, const int64_t* row_keys, const int32_t* targets,
                            const float* old_lp, uint64_t seed, float sigma, void* stream);
 
+/* Synthetic-logits keys of n active rows (device): keys[i] =
+ * (rollout_key ? rollout_key[seq[i]] : seq[i]) * 2^20 + (rows[i] - cu_seqlens[seq[i]]). */
+int prorl_row_keys(prorl_ctx* ctx, const int32_t* rows, const int32_t* seq, const int32_t* cu_seqlens,
+                   const int64_t* rollout_key, int64_t n, int64_t* keys, void* stream);
+
 /* ---- host-side helpers ------------------------------------------------------ */
 /* Per-rollout rewards [num_prompts * n] with the semantics (and, under
  * libstdc++, the exact values) of the reference's generate_workload
@@ -227,10 +232,12 @@ typedef struct prorl_host_batch {
  * before scoring it (parity mode; generation is then inside the call).
  * If `provide` is set, buffers/fill are ignored and the callback supplies each
  * micro-batch instead (the trainer's LM head): it receives the micro-batch's
- * device arrays (packed-stream row ids, targets, behaviour logprobs) and
+ * device arrays (packed-stream row ids, their sequence ids and the shard's
+ * cu_seqlens, targets, behaviour logprobs) and
  * returns a device pointer to n rows of `*row_stride` logits, stream-ordered
  * on `stream`; a non-zero return aborts the step with that status. */
 typedef int (*prorl_logits_fn)(void* user, int64_t row0, int64_t n, const int32_t* d_rows,
+                               const int32_t* d_seq, const int32_t* d_cu_seqlens,
                                const int32_t* d_targets, const float* d_old_lp,
                                const void** d_logits, int64_t* row_stride, void* stream);
 typedef struct prorl_logits_pool {

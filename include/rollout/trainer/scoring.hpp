@@ -64,11 +64,14 @@ struct ScoreResult {
 class LogitsSource {
  public:
   virtual ~LogitsSource() = default;
-  // d_rows: positions in the packed stream (row r predicts token r+1);
-  // d_targets / d_old_lp: the rows' target ids and behaviour logprobs; the
-  // micro-batch covers active rows [row0, row0 + n). Returns a device pointer
-  // to n rows of `row_stride` logits (cfg.dtype), valid until the next call.
+  // d_rows: positions in the packed stream (row r predicts token r+1), d_seq
+  // their sequence (rollout slot) ids, d_cu_seqlens the shard's sequence
+  // offsets; d_targets / d_old_lp: the rows' target ids and behaviour
+  // logprobs. The micro-batch covers active rows [row0, row0 + n). Returns a
+  // device pointer to n rows of `row_stride` logits (cfg.dtype), valid until
+  // the next call.
   virtual const void* logits(std::int64_t row0, std::int64_t n, const std::int32_t* d_rows,
+                             const std::int32_t* d_seq, const std::int32_t* d_cu_seqlens,
                              const std::int32_t* d_targets, const float* d_old_lp, std::int64_t* row_stride,
                              void* stream) = 0;
 };
@@ -79,12 +82,14 @@ class SyntheticLogits : public LogitsSource {
   SyntheticLogits(int device, int vocab, LogitsDtype dtype, std::int64_t max_rows, std::uint64_t seed,
                   float sigma = 2.0f);
   ~SyntheticLogits() override;
-  const void* logits(std::int64_t row0, std::int64_t n, const std::int32_t* d_rows, const std::int32_t* d_targets,
-                     const float* d_old_lp, std::int64_t* row_stride, void* stream) override;
+  const void* logits(std::int64_t row0, std::int64_t n, const std::int32_t* d_rows, const std::int32_t* d_seq,
+                     const std::int32_t* d_cu_seqlens, const std::int32_t* d_targets, const float* d_old_lp,
+                     std::int64_t* row_stride, void* stream) override;
 
  private:
   prorl_ctx* ctx_ = nullptr;
   void* buf_ = nullptr;
+  std::int64_t* keys_ = nullptr;  // per-row synthetic keys (seq * 2^20 + position), as the oracle
   int vocab_;
   LogitsDtype dtype_;
   std::int64_t max_rows_;

@@ -31,7 +31,7 @@ EXPORTS = [
     "prorl_abi_version", "prorl_kernel_config", "prorl_last_error", "prorl_status_code", "prorl_ctx_create", "prorl_ctx_destroy",
     "prorl_check_errors", "prorl_pack", "prorl_grpo_adv", "prorl_logprob_entropy", "prorl_clipped_loss",
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
-    "prorl_gen_logits_keyed",
+    "prorl_gen_logits_keyed", "prorl_row_keys",
     "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host",
 ]
 
@@ -89,6 +89,7 @@ def _load() -> C.CDLL:
         "prorl_allreduce": (C.c_int, [vp, vp, C.c_int, vp]),
         "prorl_gen_logits": (C.c_int, [vp, vp, C.c_int, i64, i32, i64, i64, vp, vp, u64, f32, vp]),
         "prorl_gen_logits_keyed": (C.c_int, [vp, vp, C.c_int, i64, i32, i64, vp, vp, vp, u64, f32, vp]),
+        "prorl_row_keys": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
         "prorl_synth_rewards": (C.c_int, [i32, i32, u64, f64, vp]),
         "prorl_shard_lpt": (C.c_int, [i32, vp, i32, vp]),
         "prorl_score_host": (C.c_int, [vp, C.POINTER(HostBatch), C.POINTER(ScoreCfg), C.POINTER(LogitsPool), vp, vp,

@@ -284,6 +284,13 @@ int prorl_gen_logits_keyed(prorl_ctx* c, void* logits, int dtype, int64_t row_st
                            c->n_sm, S(stream));
 }
 
+int prorl_row_keys(prorl_ctx* c, const int32_t* rows, const int32_t* seq, const int32_t* cu_seqlens,
+                   const int64_t* rollout_key, int64_t n, int64_t* keys, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_row_keys: null ctx");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_row_keys(rows, seq, cu_seqlens, rollout_key, n, keys, S(stream));
+}
+
 int prorl_shard_lpt(int32_t n_groups, const int64_t* load, int32_t world, int32_t* owner) {
   if (n_groups < 0 || world < 1 || (n_groups > 0 && (!load || !owner)))
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_shard_lpt: bad args");
@@ -397,8 +404,8 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
     const void* buf = nullptr;
     int64_t stride = pool->row_stride;
     if (pool->provide) {
-      const int rc = pool->provide(pool->user, row0, n, pk.act_row + row0, pk.act_target + row0, pk.act_old_lp + row0,
-                                   &buf, &stride, stream);
+      const int rc = pool->provide(pool->user, row0, n, pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
+                                   pk.act_target + row0, pk.act_old_lp + row0, &buf, &stride, stream);
       if (rc != PRORL_OK) return rc;
       if (!buf) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: logits callback returned null");
     } else {

@@ -53,15 +53,14 @@ template <> struct Elem<__nv_bfloat16> {
     b = b > 0xf000u ? 0xf000u : b;  // same clamp as the packed path
     return __uint_as_float(b << 16);
   }
+  // Group max (packed HMNMX2). The fast path runs unclamped: a -inf / NaN
+  // logit turns the row's T sum into NaN, which sends the row down the
+  // clamped re-read path (row_slow) instead of paying a clamp per logit.
   template <int NV>
-  __device__ static float clamp_max(uint4 (&v)[NV]) {
+  __device__ static float group_max(uint4 (&v)[NV]) {
     uint32_t m = 0;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      v[j].x = __vminu2(v[j].x, kClampWord);
-      v[j].y = __vminu2(v[j].y, kClampWord);
-      v[j].z = __vminu2(v[j].z, kClampWord);
-      v[j].w = __vminu2(v[j].w, kClampWord);
       __nv_bfloat162 a = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].x), *reinterpret_cast<__nv_bfloat162*>(&v[j].y));
       __nv_bfloat162 b = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].z), *reinterpret_cast<__nv_bfloat162*>(&v[j].w));
       a = __hmax2(a, b);
@@ -93,20 +92,20 @@ template <> struct Elem<__nv_bfloat16> {
       }
     }
   }
+  // Two logits per step on the packed fp32x2 pipe (FFMA2 / FADD2, sm_100):
+  // d = x*c - M, e = 2^d (two MUFU.EX2), S += e, T += d*e.
   template <int NV>
-  __device__ static void accumulate(const uint4 (&v)[NV], float c, float nMc, float (&S)[4], float (&Tt)[4]) {
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xffff0000u);
-        const float d0 = fmaf(x0, c, nMc), d1 = fmaf(x1, c, nMc);
-        const float e0 = ex2_approx(d0), e1 = ex2_approx(d1);
-        S[(2 * q) & 3] += e0;
-        Tt[(2 * q) & 3] = fmaf(d0, e0, Tt[(2 * q) & 3]);
-        S[(2 * q + 1) & 3] += e1;
-        Tt[(2 * q + 1) & 3] = fmaf(d1, e1, Tt[(2 * q + 1) & 3]);
+        const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+        const float2 d = __ffma2_rn(x, c2, nM2);
+        const float2 e = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+        S[q & 1] = __fadd2_rn(S[q & 1], e);
+        Tt[q & 1] = __ffma2_rn(d, e, Tt[q & 1]);
       }
     }
   }
@@ -120,18 +119,12 @@ template <> struct Elem<float> {
     return fmaxf(__ldg(reinterpret_cast<const float*>(row) + idx), kFloor);
   }
   template <int NV>
-  __device__ static float clamp_max(uint4 (&v)[NV]) {
+  __device__ static float group_max(uint4 (&v)[NV]) {
     float m = kFloor;
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      uint32_t* w = &v[j].x;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float x = fmaxf(__uint_as_float(w[q]), kFloor);
-        w[q] = __float_as_uint(x);
-        m = fmaxf(m, x);
-      }
-    }
+    for (int j = 0; j < NV; ++j)
+      m = fmaxf(m, fmaxf(fmaxf(__uint_as_float(v[j].x), __uint_as_float(v[j].y)),
+                         fmaxf(__uint_as_float(v[j].z), __uint_as_float(v[j].w))));
     return m;
   }
   template <int NV>
@@ -149,17 +142,18 @@ template <> struct Elem<float> {
     }
   }
   template <int NV>
-  __device__ static void accumulate(const uint4 (&v)[NV], float c, float nMc, float (&S)[4], float (&Tt)[4]) {
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float d = fmaf(__uint_as_float(w[q]), c, nMc);
-        const float e = ex2_approx(d);
-        S[q] += e;
-        Tt[q] = fmaf(d, e, Tt[q]);
-      }
+      const float2 xa = make_float2(__uint_as_float(v[j].x), __uint_as_float(v[j].y));
+      const float2 xb = make_float2(__uint_as_float(v[j].z), __uint_as_float(v[j].w));
+      const float2 da = __ffma2_rn(xa, c2, nM2), db = __ffma2_rn(xb, c2, nM2);
+      const float2 ea = make_float2(ex2_approx(da.x), ex2_approx(da.y));
+      const float2 eb = make_float2(ex2_approx(db.x), ex2_approx(db.y));
+      S[0] = __fadd2_rn(S[0], ea);
+      Tt[0] = __ffma2_rn(da, ea, Tt[0]);
+      S[1] = __fadd2_rn(S[1], eb);
+      Tt[1] = __ffma2_rn(db, eb, Tt[1]);
     }
   }
 };
@@ -174,27 +168,57 @@ struct Top {
 // lane's sums to the new max, turns the previous top element into an ordinary
 // term (added by lane 0), and returns the lane that holds the new top element
 // (lowest lane on ties) — that lane must exclude one copy of it from its sums.
-__device__ __forceinline__ int raise_top(float lm, float c, Top& top, float (&S)[4], float (&Tt)[4], int lane) {
+__device__ __forceinline__ int raise_top(float lm, float c, Top& top, float2 (&S)[2], float2 (&Tt)[2], int lane) {
   const float gl = warp_max(lm);
   const float nMc = gl * c;
   if (top.Mc != -INFINITY) {
     const float sc = ex2_approx(top.Mc - nMc);
     const float dl = nMc - top.Mc;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      Tt[k] = sc * fmaf(-dl, S[k], Tt[k]);
-      S[k] *= sc;
+    for (int k = 0; k < 2; ++k) {
+      Tt[k].x = sc * fmaf(-dl, S[k].x, Tt[k].x);
+      Tt[k].y = sc * fmaf(-dl, S[k].y, Tt[k].y);
+      S[k].x *= sc;
+      S[k].y *= sc;
     }
     if (lane == 0) {
       const float d = fmaf(top.Mx, c, -nMc);
       const float e = ex2_approx(d);
-      S[0] += e;
-      Tt[0] = fmaf(d, e, Tt[0]);
+      S[0].x += e;
+      Tt[0].x = fmaf(d, e, Tt[0].x);
     }
   }
   top.Mc = nMc;
   top.Mx = gl;
   return __ffs(__ballot_sync(kFull, lm == gl)) - 1;
+}
+
+// Clamped scalar re-read of one row straight from global memory (logits
+// clamped to >= -2^97, so -inf contributes exactly 0). Used only for rows whose
+// fast-path sums came out NaN. Returns by value (nothing of the caller's hot
+// loop state is address-taken, so it stays in registers).
+struct SlowRow {
+  float Mc, Mx, Sr, Tr;
+};
+template <typename T>
+__device__ __noinline__ SlowRow row_slow(const uint8_t* rp, int32_t vocab, float c, int lane) {
+  Top top{-INFINITY, 0.f};
+  float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  const float floor_v = __uint_as_float(0xf0000000u);
+  for (int32_t base = 0; base < vocab; base += 32) {
+    float x = base + lane < vocab ? Elem<T>::load(rp, base + lane) : floor_v;
+    if (__any_sync(kFull, x * c > top.Mc)) {
+      const int L = raise_top(x, c, top, S, Tt, lane);
+      if (lane == L) x = floor_v;
+    }
+    const float d = fmaf(x, c, -top.Mc);
+    const float e = ex2_approx(d);
+    S[0].x += e;
+    Tt[0].x = fmaf(d, e, Tt[0].x);
+  }
+  return SlowRow{top.Mc, top.Mx, warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y)),
+                 warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y))};
 }
 
 struct ScoreArgs {
@@ -349,7 +373,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
     if (lane == 0) xy = Elem<T>::load(rp, tgt);
 
     Top top{-INFINITY, 0.f};
-    float S[4] = {0.f, 0.f, 0.f, 0.f}, Tt[4] = {0.f, 0.f, 0.f, 0.f};
+    float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     if (head + tail > 0) {  // unaligned head / tail elements, one per lane (<= 14 of them)
       float x = __uint_as_float(0xf0000000u);  // -2^97: the clamp floor, contributes 0
       if (lane < head) x = Elem<T>::load(rp, lane);
@@ -361,8 +386,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
       }
       const float d = fmaf(x, c, -top.Mc);
       const float e = ex2_approx(d);
-      S[0] += e;
-      Tt[0] = fmaf(d, e, Tt[0]);
+      S[0].x += e;
+      Tt[0].x = fmaf(d, e, Tt[0].x);
     }
 
     for (int64_t ch = 0; ch < nchunks; ++ch) {
@@ -390,18 +415,24 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         uint4 u[SUBV];
 #pragma unroll
         for (int j = 0; j < SUBV; ++j) u[j] = v[g0 + j];
-        const float lm = Elem<T>::template clamp_max<SUBV>(u);
+        const float lm = Elem<T>::template group_max<SUBV>(u);
         if (__any_sync(kFull, lm * c > top.Mc)) {
           const int L = raise_top(lm, c, top, S, Tt, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(u, top.Mx);
         }
-        Elem<T>::template accumulate<SUBV>(u, c, -top.Mc, S, Tt);
+        Elem<T>::template accumulate<SUBV>(u, make_float2(c, c), make_float2(-top.Mc, -top.Mc), S, Tt);
       }
     }
 
     // ---- row end: merge lanes, re-add the top element analytically ----
-    float Sr = warp_sum((S[0] + S[1]) + (S[2] + S[3]));
-    float Tr = warp_sum((Tt[0] + Tt[1]) + (Tt[2] + Tt[3]));
+    float Sr = warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y));
+    float Tr = warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y));
+    if (!(Tr == Tr) || !(Sr == Sr)) {  // -inf / NaN / overflowing logits: clamped re-read (rare)
+      const SlowRow sr = row_slow<T>(rp, p.vocab, c, lane);
+      top = Top{sr.Mc, sr.Mx};
+      Sr = sr.Sr;
+      Tr = sr.Tr;
+    }
     if (lane == 0) {
       const float r = fmaf(top.Mx, c, -top.Mc);  // top element's own exponent (~0)
       const float ir = ex2_approx(-r);
@@ -519,11 +550,12 @@ __global__ void k_slab_reduce(const double* __restrict__ slab, int rows, double*
 // PRORL_K2_CONFIG (tuning) — default chosen from ncu/bench measurements.
 struct K2Config {
   const char* name;
-  int warps, stages, chunk;
+  int warps, stages, chunk, subv;  // subv: 16-B vectors per lane per max-check group (bf16: 8 logits each)
 };
-constexpr K2Config kConfigs[] = {
-    {"w16s2c4096", 16, 2, 4096}, {"w12s3c4096", 12, 3, 4096}, {"w8s5c4096", 8, 5, 4096}, {"w14s3c4096", 14, 3, 4096}};
-constexpr int kDefaultConfig = 0;
+constexpr K2Config kConfigs[] = {{"w16s2c4096g2", 16, 2, 4096, 2}, {"w16s2c4096g4", 16, 2, 4096, 4},
+                                 {"w12s3c4096g2", 12, 3, 4096, 2}, {"w8s5c4096g2", 8, 5, 4096, 2},
+                                 {"w8s3c8192g4", 8, 3, 8192, 4}};
+constexpr int kDefaultConfig = 1;
 
 int active_config() {
   static int idx = [] {
@@ -536,9 +568,9 @@ int active_config() {
   return idx;
 }
 
-template <typename T, int W, int ST, int CH, bool FUSED>
+template <typename T, int W, int ST, int CH, int SUBV_BF16, bool FUSED>
 int run_score_cfg(const ScoreArgs& a, int grid, cudaStream_t st) {
-  constexpr int SUBV = sizeof(T) == 2 ? 2 : 4;
+  constexpr int SUBV = sizeof(T) == 2 ? SUBV_BF16 : 4;
   auto kern = k_score<T, W, ST, CH, SUBV, FUSED>;
   constexpr size_t smem = score_smem_bytes<W, ST, CH, FUSED>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
@@ -555,10 +587,11 @@ int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* 
   if (FUSED && grid > slab_rows) grid = slab_rows;
   if (rows_used) *rows_used = grid;
   switch (active_config()) {
-    case 0: return run_score_cfg<T, 16, 2, 4096, FUSED>(a, grid, st);
-    case 1: return run_score_cfg<T, 12, 3, 4096, FUSED>(a, grid, st);
-    case 2: return run_score_cfg<T, 8, 5, 4096, FUSED>(a, grid, st);
-    default: return run_score_cfg<T, 14, 3, 4096, FUSED>(a, grid, st);
+    case 0: return run_score_cfg<T, 16, 2, 4096, 2, FUSED>(a, grid, st);
+    case 1: return run_score_cfg<T, 16, 2, 4096, 4, FUSED>(a, grid, st);
+    case 2: return run_score_cfg<T, 12, 3, 4096, 2, FUSED>(a, grid, st);
+    case 3: return run_score_cfg<T, 8, 5, 4096, 2, FUSED>(a, grid, st);
+    default: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, st);
   }
 }
 

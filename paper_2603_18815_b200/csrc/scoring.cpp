@@ -121,7 +121,8 @@ SyntheticLogits::SyntheticLogits(int device, int vocab, LogitsDtype dtype, std::
     : vocab_(vocab), dtype_(dtype), max_rows_(max_rows), seed_(seed), sigma_(sigma) {
   throw_status(prorl_ctx_create(device, &ctx_));
   const size_t esz = dtype == LogitsDtype::BF16 ? 2 : 4;
-  if (cudaMalloc(&buf_, (size_t)max_rows * (size_t)vocab * esz) != cudaSuccess) {
+  if (cudaMalloc(&buf_, (size_t)max_rows * (size_t)vocab * esz) != cudaSuccess ||
+      cudaMalloc(&keys_, sizeof(std::int64_t) * (size_t)max_rows) != cudaSuccess) {
     prorl_ctx_destroy(ctx_);
     throw CudaError("SyntheticLogits: cudaMalloc failed");
   }
@@ -129,14 +130,18 @@ SyntheticLogits::SyntheticLogits(int device, int vocab, LogitsDtype dtype, std::
 
 SyntheticLogits::~SyntheticLogits() {
   if (buf_) cudaFree(buf_);
+  if (keys_) cudaFree(keys_);
   prorl_ctx_destroy(ctx_);
 }
 
-const void* SyntheticLogits::logits(std::int64_t row0, std::int64_t n, const std::int32_t*, const std::int32_t* d_targets,
-                                    const float* d_old_lp, std::int64_t* row_stride, void* stream) {
+const void* SyntheticLogits::logits(std::int64_t, std::int64_t n, const std::int32_t* d_rows,
+                                    const std::int32_t* d_seq, const std::int32_t* d_cu_seqlens,
+                                    const std::int32_t* d_targets, const float* d_old_lp, std::int64_t* row_stride,
+                                    void* stream) {
   if (n > max_rows_) throw ShapeMismatch("SyntheticLogits: micro-batch larger than max_rows");
-  throw_status(prorl_gen_logits(ctx_, buf_, (int)dtype_, vocab_, vocab_, n, row0, d_targets, d_old_lp, seed_, sigma_,
-                                stream));
+  throw_status(prorl_row_keys(ctx_, d_rows, d_seq, d_cu_seqlens, nullptr, n, keys_, stream));
+  throw_status(prorl_gen_logits_keyed(ctx_, buf_, (int)dtype_, vocab_, vocab_, n, keys_, d_targets, d_old_lp, seed_,
+                                      sigma_, stream));
   *row_stride = vocab_;
   return buf_;
 }
@@ -164,11 +169,11 @@ struct Trampoline {
 };
 
 int provide_logits(void* user, std::int64_t row0, std::int64_t n, const std::int32_t* d_rows,
-                   const std::int32_t* d_targets, const float* d_old_lp, const void** d_logits,
-                   std::int64_t* row_stride, void* stream) {
+                   const std::int32_t* d_seq, const std::int32_t* d_cu_seqlens, const std::int32_t* d_targets,
+                   const float* d_old_lp, const void** d_logits, std::int64_t* row_stride, void* stream) {
   auto* t = static_cast<Trampoline*>(user);
   try {
-    *d_logits = t->src->logits(row0, n, d_rows, d_targets, d_old_lp, row_stride, stream);
+    *d_logits = t->src->logits(row0, n, d_rows, d_seq, d_cu_seqlens, d_targets, d_old_lp, row_stride, stream);
     return PRORL_OK;
   } catch (const Error& e) {
     t->error = e.code() + ": " + e.what();

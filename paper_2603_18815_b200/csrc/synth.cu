@@ -14,22 +14,20 @@ __global__ void k_gen_logits(uint8_t* __restrict__ out, int64_t row_stride, int3
                              int64_t row_key0, const int64_t* __restrict__ row_keys,
                              const int32_t* __restrict__ targets,
                              const float* __restrict__ old_lp, uint32_t s0, float scale, float base) {
-  const int64_t total = n_rows * (int64_t)vocab;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx / vocab;
-    const int32_t col = (int32_t)(idx - i * vocab);
+  // one CTA per row (grid-strided), threads across the vocabulary: no 64-bit division
+  for (int64_t i = blockIdx.x; i < n_rows; i += gridDim.x) {
     const uint64_t row_key = row_keys ? (uint64_t)row_keys[i] : (uint64_t)(row_key0 + i);
-    float x;
-    if (old_lp != nullptr && targets[i] == col)
-      x = prorl_plant_logit(row_key, s0, base, old_lp[i]);
-    else
-      x = prorl_noise_logit(row_key * (uint64_t)vocab + (uint64_t)col, s0, scale);
-    const int64_t o = i * row_stride + col;
-    if (BF16) {
-      reinterpret_cast<uint16_t*>(out)[o] = prorl_f32_to_bf16_bits(x);
-    } else {
-      reinterpret_cast<float*>(out)[o] = x;
+    const int32_t tgt = old_lp != nullptr ? targets[i] : -1;
+    const float plant = old_lp != nullptr ? prorl_plant_logit(row_key, s0, base, old_lp[i]) : 0.f;
+    const uint64_t key0 = row_key * (uint64_t)vocab;
+    for (int32_t col = threadIdx.x; col < vocab; col += blockDim.x) {
+      const float x = col == tgt ? plant : prorl_noise_logit(key0 + (uint64_t)col, s0, scale);
+      const int64_t o = i * row_stride + col;
+      if (BF16) {
+        reinterpret_cast<uint16_t*>(out)[o] = prorl_f32_to_bf16_bits(x);
+      } else {
+        reinterpret_cast<float*>(out)[o] = x;
+      }
     }
   }
 }
