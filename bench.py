@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--pool", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-backward", action="store_true")
     return ap.parse_args()
 
 
@@ -142,6 +143,37 @@ def cpu_baseline(shard, cfg, seed: int, budget_s: float) -> dict:
             "sample": f"first {n} of {shard.n_active} active rows of the same shard (scoring time; logits "
                       f"generation excluded; pack+GRPO of the full shard amortised pro rata)",
             "seconds": float(r["timings"][1])}
+
+
+def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
+    """K5 (dL/dlogits, SURVEY §8 f rank 1) on one full logits micro-batch:
+    reads pool[0] (2V B/row), writes the bf16 gradient into pool[1] (2V B/row).
+    Not part of the forward metric; reported beside it."""
+    import torch
+    from paper_2603_18815_b200.hotpath import LossConfig
+    n, V = pool[0].shape
+    g = torch.Generator(device="cuda").manual_seed(7)
+    targets = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
+    logp, _ = sc.logprob_entropy(pool[0], targets)
+    old = logp + 0.3 * (torch.rand(n, device="cuda", generator=g) - 0.5)
+    adv = torch.randn(64, device="cuda", generator=g)
+    seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
+    for _ in range(2):
+        sc.logits_grad(pool[0], targets, logp, old, adv, seq, float(n), grad=pool[1])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        sc.logits_grad(pool[0], targets, logp, old, adv, seq, float(n), grad=pool[1])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    bpr = 2 * V * (2 if c["dtype"] == "bf16" else 4) + 26
+    gbs = n * bpr / (ms / 1e3) / 1e9
+    peak, kind = measured_peak_gbs()
+    return {"kernel": "k_grad (K5: dL/dlogits, bf16 out)", "rows_per_launch": n, "ms_per_launch": ms,
+            "rows_per_s": n / (ms / 1e3), "bytes_per_row": bpr, "achieved_gbs": gbs, "frac_of_measured": gbs / peak,
+            "frac_of_nominal_8000": gbs / 8000.0}
 
 
 def run_reference(args):
@@ -239,6 +271,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and not args.no_backward else None
     e2e_ms = ev0.elapsed_time(ev1)
     dev_ms = float(seg[1] + seg[2] + seg[3])  # pack+GRPO, score, all-reduce (inputs resident)
     score_ms = float(seg[2])
@@ -296,6 +329,7 @@ def run_ours(args):
             "result": {"loss": res["loss"], "entropy": res["entropy"], "clip_lo_frac": res["clip_lo_frac"],
                        "clip_hi_frac": res["clip_hi_frac"], "n_active": res["n_active"]},
             "cpu_baseline": cpu,
+            "backward": backward,
         }
         print(json.dumps(line), flush=True)
     sc.close()

@@ -176,6 +176,20 @@ int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_
                      const prorl_loss_cfg* cfg, float* logp, float* entropy,
                      double* partials_dev, void* stream);
 
+/* ---- K5: backward through the log-softmax (SURVEY §8 f rank 1) -------------- */
+/* Writes dL/dlogits for the DAPO token-mean surrogate L = sum_i l_i / n_global:
+ * grad[i][v] = g_i * inv_temp * (1[v = y_i] - softmax(x_i inv_temp)_v), with
+ * g_i = -A ratio / n_global when the unclipped branch is the min, else 0, and
+ * the row's lse recovered as x_y inv_temp - logp_i (logp from K2). grad rows
+ * are addressed like the logits rows (rows[] indirection, same row_stride,
+ * same 16-B phase); grad may alias logits (in place). dtype of grad = dtype
+ * of logits. dlogp (nullable) receives g_i. */
+int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                      const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
+                      const float* adv, const int32_t* row_seq, int64_t n_rows, float inv_temp,
+                      const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
+                      float* dlogp, void* stream);
+
 /* ---- NCCL ------------------------------------------------------------------ */
 /* 128-byte ncclUniqueId produced on rank 0, broadcast by the caller. */
 int prorl_nccl_unique_id(uint8_t* id128);

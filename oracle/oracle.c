@@ -312,6 +312,38 @@ void oracle_loss(const double* logp, const double* ent, const float* old_lp, con
              abs_partials, n_border);
 }
 
+/* ---- K5: backward through the log-softmax (SURVEY §8 f rank 1) ------------------------ */
+
+/* grad[i][v] = g_i * invT * (1[v=y] - p_v), g_i = -A ratio / n_global if the
+ * unclipped branch is the min (B.4), else 0; fp64 from the oracle's own logp.
+ * border[i] = 1 when the clip decision is within 1e-5 of flipping. */
+void oracle_logits_grad(const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
+                        const int32_t* targets, const float* old_lp, const double* adv, const int32_t* row_seq,
+                        int64_t n_rows, float inv_temp, float eps_lo, float eps_hi, double n_global, double* grad,
+                        double* dlogp, uint8_t* border) {
+  const size_t es = dtype == PRORL_BF16 ? 2 : 4;
+  const double it = (double)inv_temp, lo = 1.0 - (double)eps_lo, hi = 1.0 + (double)eps_hi;
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const int64_t r = rows ? rows[i] : i;
+    const char* row = (const char*)logits + (size_t)r * row_stride * es;
+    double lp, ent;
+    oracle_row_logprob(row, dtype, vocab, targets[i], inv_temp, &lp, &ent);
+    const double lse = logit_at(row, dtype, targets[i]) * it - lp;
+    const double A = adv[row_seq[i]];
+    const double ratio = exp(lp - (double)old_lp[i]);
+    const double pg1 = ratio * A, pg2 = (ratio < lo ? lo : (ratio > hi ? hi : ratio)) * A;
+    const double g = pg1 <= pg2 ? -A * ratio / n_global : 0.0;
+    if (dlogp) dlogp[i] = g;
+    if (border) border[i] = (fabs(ratio - lo) <= 1e-5 * lo || fabs(ratio - hi) <= 1e-5 * hi) ? 1 : 0;
+    double* gr = grad + (size_t)i * vocab;
+    for (int32_t v = 0; v < vocab; ++v) {
+      const double x = logit_at(row, dtype, v) * it;
+      const double pv = x == -INFINITY ? 0.0 : exp(x - lse);
+      gr[v] = g * it * ((v == targets[i] ? 1.0 : 0.0) - pv);
+    }
+  }
+}
+
 /* ---- full CPU path ------------------------------------------------------------------- */
 
 typedef struct {

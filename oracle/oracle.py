@@ -88,6 +88,8 @@ def lib() -> C.CDLL:
             "oracle_logprob_entropy": (None, [vp, C.c_int, i64, i32, vp, vp, i64, f32, vp, vp]),
             "oracle_loss": (None, [vp, vp, vp, vp, vp, vp, i64, f32, f32, C.c_int, vp, vp, vp]),
             "oracle_score_batch": (C.c_int, [vp, vp, u64, f32, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+            "oracle_logits_grad": (None, [vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, i64, f32, f32, f32, f64, vp, vp,
+                                          vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -184,6 +186,24 @@ def loss(logp, ent, old_lp, adv, row_seq, row_turn, eps_lo=0.2, eps_hi=0.28, n_b
                       _p(np.ascontiguousarray(row_seq, np.int32)), _p(np.ascontiguousarray(row_turn, np.int16)),
                       len(logp), eps_lo, eps_hi, n_buckets, _p(P), _p(Q), C.byref(nb))
     return P, Q, nb.value
+
+
+def logits_grad(logits: np.ndarray, targets, old_lp, adv, row_seq, n_global, rows=None, inv_temp=1.0, eps_lo=0.2,
+                eps_hi=0.28, vocab=None):
+    """Oracle dL/dlogits (fp64) [n_rows x V], dL/dlogp [n_rows], border flags [n_rows]."""
+    dtype = 0 if logits.dtype == np.uint16 else 1
+    V = vocab or logits.shape[1]
+    t = np.ascontiguousarray(targets, np.int32)
+    n = len(t)
+    g = np.zeros((n, V))
+    dl = np.zeros(n)
+    bd = np.zeros(n, np.uint8)
+    r = None if rows is None else np.ascontiguousarray(rows, np.int32)
+    lib().oracle_logits_grad(_p(logits), dtype, logits.shape[1], V, _p(r), _p(t),
+                             _p(np.ascontiguousarray(old_lp, np.float32)), _p(np.ascontiguousarray(adv, np.float64)),
+                             _p(np.ascontiguousarray(row_seq, np.int32)), n, inv_temp, eps_lo, eps_hi, n_global, _p(g),
+                             _p(dl), _p(bd))
+    return g, dl, bd
 
 
 def score_batch(hb_c, cfg_c, seed: int, sigma: float, nthreads: int = 1, row_begin: int = -1, row_end: int = -1,

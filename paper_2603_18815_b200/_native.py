@@ -31,7 +31,7 @@ EXPORTS = [
     "prorl_abi_version", "prorl_kernel_config", "prorl_last_error", "prorl_status_code", "prorl_ctx_create", "prorl_ctx_destroy",
     "prorl_check_errors", "prorl_pack", "prorl_grpo_adv", "prorl_logprob_entropy", "prorl_clipped_loss",
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
-    "prorl_gen_logits_keyed", "prorl_row_keys",
+    "prorl_gen_logits_keyed", "prorl_row_keys", "prorl_logits_grad",
     "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host",
 ]
 
@@ -84,6 +84,8 @@ def _load() -> C.CDLL:
         "prorl_clipped_loss": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(LossCfg), vp, vp]),
         "prorl_score_rows": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32,
                                        C.POINTER(LossCfg), vp, vp, vp, vp]),
+        "prorl_logits_grad": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32,
+                                        C.POINTER(LossCfg), f64, vp, i64, vp, vp]),
         "prorl_nccl_unique_id": (C.c_int, [vp]),
         "prorl_nccl_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "prorl_allreduce": (C.c_int, [vp, vp, C.c_int, vp]),

@@ -226,6 +226,17 @@ int prorl_score_rows(prorl_ctx* c, const void* logits, int dtype, int64_t row_st
   return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
 }
 
+int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                      const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
+                      const float* adv, const int32_t* row_seq, int64_t n_rows, float inv_temp,
+                      const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride, float* dlogp,
+                      void* stream) {
+  if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_logits_grad: null ctx/cfg");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_grad(c, logits, dtype, row_stride, vocab, rows, targets, logp, old_lp, adv, row_seq, n_rows, inv_temp,
+                     cfg, n_global, grad, grad_stride, dlogp, S(stream));
+}
+
 int prorl_nccl_unique_id(uint8_t* id128) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   PRORL_NCCL_API();

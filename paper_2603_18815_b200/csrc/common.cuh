@@ -90,6 +90,10 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp,
                 const float* adv, const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows,
                 const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used, cudaStream_t st);
+int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
+                const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
+                const int32_t* row_seq, int64_t n_rows, float inv_temp, const prorl_loss_cfg* cfg, double n_global,
+                void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st);
 int launch_slab_reduce(const double* slab, int slab_rows, double* partials, cudaStream_t st);
 int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
                       int64_t row_key0, const int64_t* row_keys, const int32_t* targets, const float* old_lp, uint64_t seed,

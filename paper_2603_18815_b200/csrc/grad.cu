@@ -1,0 +1,209 @@
+// grad.cu — K5: backward of the DAPO token-mean surrogate through the
+// log-softmax, streamed over the logits (SURVEY.md §8 f rank 1; no reference
+// code: SPEC.md:741).
+//
+// For active row i with target y, forward logp_i (from K2), behaviour logprob
+// old_i and advantage A = adv[seq_i]:
+//   ratio = exp(logp - old),  l = -min(ratio A, clip(ratio, 1-eps_lo, 1+eps_hi) A)
+//   dL/dlogp_i = -A ratio / N   if the unclipped branch is the min, else 0
+//                (L = sum_i l_i / N, N = global active rows after the all-reduce)
+//   dL/dx_iv   = dL/dlogp_i * inv_T * (1[v = y] - p_v),   p_v = exp(x_v inv_T - lse_i)
+// with lse_i = x_y inv_T - logp_i recovered from the forward output. One HBM
+// read + one HBM write of the row (4V bytes bf16); the same per-warp TMA ring
+// as K2 feeds the reads, results leave as 16-B streaming stores (st.global.cs)
+// packed to bf16 pairs (cvt.rn.bf16x2.f32). Rows whose gradient scale is 0
+// (clipped branch, A = 0) skip the exp work and store zeros. The gradient
+// buffer may alias the logits (in-place backward): every chunk is in shared
+// memory before its region is overwritten, and the target logit is read at
+// row start.
+#include "common.cuh"
+#include "stream.cuh"
+
+namespace prorl {
+
+namespace {
+
+constexpr float kLog2e = 1.44269504088896340736f;
+
+struct GradArgs {
+  const uint8_t* logits;
+  int64_t stride_bytes;
+  int32_t vocab;
+  const int32_t* rows;
+  uint8_t* grad;  // same row stride and 16-B phase as logits
+  const int32_t* targets;
+  const float* logp;
+  const float* old_lp;
+  const float* adv;
+  const int32_t* row_seq;
+  int64_t n_rows;
+  float c;         // inv_temp * log2 e
+  float inv_temp;
+  float lo, hi;    // 1 - eps_lo, 1 + eps_hi
+  float inv_n;     // 1 / N_global
+  float* dlogp;    // optional per-row dL/dlogp
+};
+
+template <typename T> struct GElem;
+template <> struct GElem<__nv_bfloat16> {
+  static constexpr int ES = 2;
+  __device__ static float load(const uint8_t* row, int64_t i) {
+    return __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(row) + i)) << 16);
+  }
+  __device__ static void store(uint8_t* row, int64_t i, float g) {
+    reinterpret_cast<__nv_bfloat16*>(row)[i] = __float2bfloat16_rn(g);
+  }
+  // 8 logits in, 8 gradients out (scale s = -dL/dlogp * inv_T, base-2 lse l2)
+  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+      const float2 d = __ffma2_rn(x, c2, nl2);
+      const float2 p = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+      const float2 g = __fmul2_rn(p, s2);
+      const __nv_bfloat162 b = __float22bfloat162_rn(g);
+      w[q] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <> struct GElem<float> {
+  static constexpr int ES = 4;
+  __device__ static float load(const uint8_t* row, int64_t i) { return __ldg(reinterpret_cast<const float*>(row) + i); }
+  __device__ static void store(uint8_t* row, int64_t i, float g) { reinterpret_cast<float*>(row)[i] = g; }
+  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
+    const float2 da = __ffma2_rn(make_float2(__uint_as_float(v.x), __uint_as_float(v.y)), c2, nl2);
+    const float2 db = __ffma2_rn(make_float2(__uint_as_float(v.z), __uint_as_float(v.w)), c2, nl2);
+    const float2 ga = __fmul2_rn(make_float2(ex2_approx(da.x), ex2_approx(da.y)), s2);
+    const float2 gb = __fmul2_rn(make_float2(ex2_approx(db.x), ex2_approx(db.y)), s2);
+    return make_uint4(__float_as_uint(ga.x), __float_as_uint(ga.y), __float_as_uint(gb.x), __float_as_uint(gb.y));
+  }
+};
+
+template <typename T, int WARPS, int STAGES, int CHUNK>
+__global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
+  constexpr int NV = CHUNK / 512;
+  constexpr int ES = GElem<T>::ES;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  RowRing<STAGES, CHUNK, ES> rr;
+  rr.init(smem + (size_t)warp * STAGES * CHUNK,
+          reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CHUNK) + warp * STAGES, p.logits,
+          p.stride_bytes, p.rows, p.n_rows, p.vocab, gw, nw, lane);
+  const int64_t goff = p.grad - p.logits;  // same stride and 16-B phase (checked on the host)
+
+  for (int64_t i = gw; i < p.n_rows; i += nw) {
+    const uint8_t* rp = rr.row_ptr(i);
+    uint8_t* gp = const_cast<uint8_t*>(rp) + goff;
+    uintptr_t a, b;
+    rr.interior(rp, a, b);
+    const int64_t nchunks = rr.chunks(a, b);
+    const int head = (int)((a - reinterpret_cast<uintptr_t>(rp)) / ES);
+    const int tail = (int)((reinterpret_cast<uintptr_t>(rp) + (uintptr_t)p.vocab * ES - b) / ES);
+    const int32_t y = p.targets[i];
+    // per-row scale (lane 0), broadcast
+    float s = 0.f, l2 = 0.f, xy = 0.f;
+    if (lane == 0) {
+      xy = GElem<T>::load(rp, y);
+      const float lp = p.logp[i], old = p.old_lp[i];
+      const float A = p.adv[p.row_seq[i]];
+      const float ratio = expf(lp - old);
+      const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
+      const float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
+      if (p.dlogp) p.dlogp[i] = dl;
+      s = -dl * p.inv_temp;  // grad_v = s * p_v for v != y, grad_y = -s * (1 - p_y)
+      l2 = fmaf(xy, p.c, -lp * kLog2e);                            // lse in base-2 units
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
+    l2 = __shfl_sync(0xffffffffu, l2, 0);
+    xy = __shfl_sync(0xffffffffu, xy, 0);
+    const float2 c2 = make_float2(p.c, p.c), nl2 = make_float2(-l2, -l2), s2 = make_float2(s, s);
+    const bool zero = (s == 0.f);  // warp-uniform: clipped branch / A == 0 -> all-zero row
+
+    if (head + tail > 0) {
+      int64_t idx = -1;
+      if (lane < head) idx = lane;
+      else if (lane < head + tail) idx = (int64_t)((b - reinterpret_cast<uintptr_t>(rp)) / ES) + (lane - head);
+      if (idx >= 0) {
+        const float x = GElem<T>::load(rp, idx);
+        GElem<T>::store(gp, idx, zero ? 0.f : s * ex2_approx(fmaf(x, p.c, -l2)));
+      }
+    }
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const uint32_t nvec = (uint32_t)(min((uintptr_t)CHUNK, b - (a + (uintptr_t)ch * CHUNK)) >> 4);
+      const uint4* sv = rr.wait();
+      uint4 v[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const uint32_t q = lane + 32 * j;
+        v[j] = q < nvec ? sv[q] : make_uint4(0, 0, 0, 0);
+      }
+      rr.release(lane);
+      uint4* dst = reinterpret_cast<uint4*>(a + (uintptr_t)ch * CHUNK + (uintptr_t)goff);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const uint32_t q = lane + 32 * j;
+        if (q < nvec) __stcs(dst + q, zero ? make_uint4(0, 0, 0, 0) : GElem<T>::vec(v[j], c2, nl2, s2));
+      }
+    }
+    __syncwarp();  // order the row's vector stores before the target fix-up
+    if (lane == 0) {
+      const float py = ex2_approx(fmaf(xy, p.c, -l2));
+      GElem<T>::store(gp, y, -s * (1.f - py));
+    }
+  }
+}
+
+constexpr int kGradWarps = 16, kGradStages = 2, kGradChunk = 4096;
+
+template <typename T>
+int run_grad(const GradArgs& a, int n_sm, cudaStream_t st) {
+  auto kern = k_grad<T, kGradWarps, kGradStages, kGradChunk>;
+  constexpr size_t smem = (size_t)kGradWarps * kGradStages * kGradChunk + (size_t)kGradWarps * kGradStages * 8;
+  PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::min<int64_t>((int64_t)n_sm, (a.n_rows + kGradWarps - 1) / kGradWarps);
+  kern<<<grid, kGradWarps * 32, smem, st>>>(a);
+  PRORL_CUDA(cudaGetLastError());
+  return PRORL_OK;
+}
+
+}  // namespace
+
+int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
+                const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
+                const int32_t* row_seq, int64_t n_rows, float inv_temp, const prorl_loss_cfg* cfg, double n_global,
+                void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st) {
+  if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "logits_grad: unknown dtype");
+  if (vocab <= 0 || row_stride < vocab) return fail(PRORL_E_SHAPE, "logits_grad: need vocab > 0, row_stride >= vocab");
+  if (grad_stride != row_stride)
+    return fail(PRORL_E_SHAPE, "logits_grad: grad_stride must equal row_stride (in-place or same layout)");
+  const int esz = dtype == PRORL_BF16 ? 2 : 4;
+  const intptr_t delta = static_cast<const uint8_t*>(grad) - static_cast<const uint8_t*>(logits);
+  if (reinterpret_cast<uintptr_t>(logits) % esz || (delta % 16) != 0)
+    return fail(PRORL_E_SHAPE, "logits_grad: grad must have the logits' 16-byte alignment phase");
+  if (!(inv_temp > 0.f) || !(n_global > 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "logits_grad: bad inv_temp/n_global");
+  if (n_rows <= 0) return PRORL_OK;
+  GradArgs a{};
+  a.logits = static_cast<const uint8_t*>(logits);
+  a.stride_bytes = row_stride * esz;
+  a.vocab = vocab;
+  a.rows = rows;
+  a.grad = static_cast<uint8_t*>(grad);
+  a.targets = targets;
+  a.logp = logp;
+  a.old_lp = old_lp;
+  a.adv = adv;
+  a.row_seq = row_seq;
+  a.n_rows = n_rows;
+  a.c = inv_temp * kLog2e;
+  a.inv_temp = inv_temp;
+  a.lo = 1.0f - cfg->eps_lo;
+  a.hi = 1.0f + cfg->eps_hi;
+  a.inv_n = (float)(1.0 / n_global);
+  a.dlogp = dlogp;
+  return dtype == PRORL_BF16 ? run_grad<__nv_bfloat16>(a, ctx->n_sm, st) : run_grad<float>(a, ctx->n_sm, st);
+}
+
+}  // namespace prorl

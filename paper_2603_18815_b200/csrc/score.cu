@@ -34,6 +34,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "stream.cuh"
 
 namespace prorl {
 
@@ -294,78 +295,25 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
   double* g_w = reinterpret_cast<double*>(smem + (size_t)WARPS * STAGES * CHUNK + WARPS * STAGES * 8);
   double* bk_w = g_w + WARPS * kNG;
 
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
   double g[kNG];
   if constexpr (FUSED) {
 #pragma unroll
     for (int k = 0; k < kNG; ++k) g[k] = 0.0;
     for (int i = lane; i < kBucketDoubles; i += 32) bk_w[warp * kBucketDoubles + i] = 0.0;
   }
-  __syncwarp();
 
   const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  const uint64_t policy = l2_policy_evict_first();
+  RowRing<STAGES, CHUNK, ES> rr;
+  rr.init(ring, bars, p.logits, p.stride_bytes, p.rows, p.n_rows, p.vocab, gw, nw, lane);
 
-  auto row_ptr = [&](int64_t i) -> const uint8_t* {
-    const int64_t r = p.rows ? (int64_t)p.rows[i] : i;
-    return p.logits + r * p.stride_bytes;
-  };
-  // interior [a, b) of a row: 16-B aligned, multiple of 16 bytes.
-  auto interior = [&](const uint8_t* rp, uintptr_t& a, uintptr_t& b) {
-    const uintptr_t st = reinterpret_cast<uintptr_t>(rp);
-    const uintptr_t en = st + (uintptr_t)p.vocab * ES;
-    a = (st + 15) & ~(uintptr_t)15;
-    if (a > en) a = en;
-    b = en & ~(uintptr_t)15;
-    if (b < a) b = a;
-  };
-
-  // ---- producer state (meaningful in lane 0 only) ----
-  int64_t p_row = gw;
-  int64_t p_chunk = 0, p_nchunks = 0;
-  uintptr_t p_a = 0, p_b = 0;
-  uint32_t produced = 0;
-  if (p_row < p.n_rows) {
-    interior(row_ptr(p_row), p_a, p_b);
-    p_nchunks = (int64_t)((p_b - p_a + CHUNK - 1) / CHUNK);
-  }
-  auto produce = [&]() {
-    while (p_row < p.n_rows && p_chunk >= p_nchunks) {
-      p_row += nw;
-      p_chunk = 0;
-      p_nchunks = 0;
-      if (p_row < p.n_rows) {
-        interior(row_ptr(p_row), p_a, p_b);
-        p_nchunks = (int64_t)((p_b - p_a + CHUNK - 1) / CHUNK);
-      }
-    }
-    if (p_row >= p.n_rows) return;
-    const uintptr_t src = p_a + (uintptr_t)p_chunk * CHUNK;
-    const uint32_t bytes = (uint32_t)min((uintptr_t)CHUNK, p_b - src);
-    const int s = produced % STAGES;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&bars[s], bytes);
-    tma_load_1d(ring + (size_t)s * CHUNK, reinterpret_cast<const void*>(src), bytes, &bars[s], policy);
-    ++produced;
-    ++p_chunk;
-  };
-  if (lane == 0) {
-    for (int s = 0; s < STAGES; ++s) produce();
-  }
-
-  uint32_t consumed = 0;
   const float c = p.c;
   const uint4 fill = make_uint4(Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord);
   for (int64_t i = gw; i < p.n_rows; i += nw) {
-    const uint8_t* rp = row_ptr(i);
+    const uint8_t* rp = rr.row_ptr(i);
     uintptr_t a, b;
-    interior(rp, a, b);
-    const int64_t nchunks = (int64_t)((b - a + CHUNK - 1) / CHUNK);
+    rr.interior(rp, a, b);
+    const int64_t nchunks = rr.chunks(a, b);
     const int head = (int)((a - reinterpret_cast<uintptr_t>(rp)) / ES);
     const int tail = (int)((reinterpret_cast<uintptr_t>(rp) + (uintptr_t)p.vocab * ES - b) / ES);
     const int32_t tgt = p.targets[i];
@@ -391,11 +339,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
     }
 
     for (int64_t ch = 0; ch < nchunks; ++ch) {
-      const int s = consumed % STAGES;
-      const uint32_t parity = (consumed / STAGES) & 1;
       const uint32_t nvec = (uint32_t)(min((uintptr_t)CHUNK, b - (a + (uintptr_t)ch * CHUNK)) >> 4);
-      mbar_wait(&bars[s], parity);
-      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * CHUNK);
+      const uint4* sv = rr.wait();
       uint4 v[NV];
       if (nvec == (uint32_t)(CHUNK / 16)) {
 #pragma unroll
@@ -407,9 +352,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
           v[j] = q < nvec ? sv[q] : fill;
         }
       }
-      __syncwarp();
-      ++consumed;
-      if (lane == 0) produce();
+      rr.release(lane);
 #pragma unroll
       for (int g0 = 0; g0 < NV; g0 += SUBV) {
         uint4 u[SUBV];

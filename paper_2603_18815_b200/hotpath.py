@@ -147,6 +147,23 @@ class Scorer:
                                      C.byref(c), ptr(logp), ptr(ent), ptr(partials), _stream(stream)))
         return partials, logp, ent
 
+    # ---- K5: backward through the log-softmax ----
+    def logits_grad(self, logits, targets, logp, old_lp, adv, row_seq, n_global: float, rows=None,
+                    inv_temp: float = 1.0, cfg: LossConfig | None = None, grad=None, vocab: int | None = None,
+                    want_dlogp: bool = False, stream=None):
+        """dL/dlogits (same dtype/layout as logits; grad=logits for in place)."""
+        if grad is None:
+            grad = torch.empty_like(logits)
+        n = targets.numel()
+        dl = torch.empty(n, dtype=torch.float32, device=targets.device) if want_dlogp else None
+        c = (cfg or LossConfig()).c()
+        V = vocab if vocab is not None else logits.shape[1]
+        check(N.lib.prorl_logits_grad(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
+                                      ptr(targets), ptr(logp), ptr(old_lp), ptr(adv), ptr(row_seq), n, inv_temp,
+                                      C.byref(c), float(n_global), ptr(grad), grad.stride(0), ptr(dl),
+                                      _stream(stream)))
+        return grad, dl
+
     # ---- synthetic LM head ----
     def gen_logits(self, out: torch.Tensor, n_rows: int, row_key0: int, targets=None, old_lp=None, seed: int = 0,
                    sigma: float = 2.0, vocab: int | None = None, stream=None) -> torch.Tensor:
