@@ -172,6 +172,20 @@ class Scorer:
                                      ptr(targets), ptr(old_lp), seed, sigma, _stream(stream)))
         return out
 
+    def row_keys(self, rows, seq, cu_seqlens, rollout_key=None, stream=None) -> torch.Tensor:
+        """Synthetic-logits keys of active rows (rollout_key[seq] * 2^20 + position)."""
+        keys = torch.empty(max(rows.numel(), 1), dtype=torch.int64, device=rows.device)
+        check(N.lib.prorl_row_keys(self.ctx, ptr(rows), ptr(seq), ptr(cu_seqlens), ptr(rollout_key), rows.numel(),
+                                   ptr(keys), _stream(stream)))
+        return keys[:rows.numel()]
+
+    def gen_logits_keyed(self, out: torch.Tensor, keys: torch.Tensor, targets=None, old_lp=None, seed: int = 0,
+                         sigma: float = 2.0, vocab: int | None = None, stream=None) -> torch.Tensor:
+        V = vocab if vocab is not None else out.shape[1]
+        check(N.lib.prorl_gen_logits_keyed(self.ctx, ptr(out), _DT[out.dtype], out.stride(0), V, keys.numel(),
+                                           ptr(keys), ptr(targets), ptr(old_lp), seed, sigma, _stream(stream)))
+        return out
+
     # ---- NCCL ----
     def nccl_init(self, world: int, rank: int, uid: bytes) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
