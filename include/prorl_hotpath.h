@@ -239,6 +239,28 @@ typedef struct prorl_host_batch {
                                * (synthetic-logits key; NULL = slot index) */
 } prorl_host_batch;
 
+/* ---- trajectory ingestion (SURVEY §8 f rank 3) ------------------------------ */
+/* Parses /process responses — the reference's wire schema,
+ * build_process_response (proj/src/handlers.cpp:57-91) — straight into a
+ * shard's host SoA, with the reference's participation rules: turns validated
+ * as TokenTrajectory::validate (MalformedTurn), FAILED rollouts not usable and
+ * groups failing is_informative(tolerance) contributing empty sequences
+ * (proj/src/trainer/harness.cpp:84-102). Responses are in shard order: group g
+ * owns responses [group_off[g], group_off[g+1]), group_off[0] = 0; rollout
+ * slot (seq id) = response index. n_threads < 1: all host threads.
+ * out->batch points into library-owned memory until prorl_ingest_free. */
+typedef struct prorl_ingest_result {
+  prorl_host_batch batch;
+  int64_t n_active;
+  int32_t n_informative;
+  int32_t pad_;
+  void* impl;
+} prorl_ingest_result;
+int prorl_ingest_responses(const char* const* json, const size_t* len, const int32_t* group_off,
+                           int32_t n_groups, double gate_tolerance, int32_t n_threads,
+                           prorl_ingest_result* out);
+int prorl_ingest_free(prorl_ingest_result* r);
+
 /* Logits provider for prorl_score_host: micro-batch j (active rows
  * [row0, row0+n)) reads logits from pool[j % n_pool] (each buffer holds
  * >= microbatch_rows rows of row_stride elements). If `fill` is non-zero the

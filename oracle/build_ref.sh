@@ -30,7 +30,8 @@ fi
 mkdir -p "$OUT/obj"
 CXX="${CXX:-g++}"
 FLAGS=(-std=c++20 -O2 -fPIC -I"$REF/include" -I"$JSON_DIR")
-for src in src/trainer/harness.cpp src/trainer/workload.cpp src/mock/policy.cpp; do
+for src in src/trainer/harness.cpp src/trainer/workload.cpp src/mock/policy.cpp src/handlers.cpp \
+           src/sandbox/build_cache.cpp src/sandbox/framing.cpp src/sandbox/proc.cpp src/sandbox/runtime.cpp; do
   "$CXX" "${FLAGS[@]}" -c "$REF/$src" -o "$OUT/obj/$(basename "$src" .cpp).o"
 done
 "$CXX" "${FLAGS[@]}" -c "$HERE/ref_shim.cpp" -o "$OUT/obj/ref_shim.o"

@@ -114,6 +114,7 @@ def ref_lib() -> C.CDLL | None:
         "ref_token_logprob": (f64, [i64]),
         "ref_prompt_digest": (u64, [vp, i64]),
         "ref_generate_workload_rewards": (C.c_int, [C.c_int, C.c_int, u64, f64, vp]),
+        "ref_process_response": (i64, [C.c_char_p, C.c_int, vp, vp, vp, vp, f64, C.c_int, C.c_char_p, vp, i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

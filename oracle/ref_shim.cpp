@@ -8,12 +8,16 @@
 //   ref_usable_rewards / ref_is_informative -> harness.cpp:84-102
 //   ref_fnv1a64 / ref_hash_token / ref_token_logprob -> mock/policy.cpp:10-53
 //   ref_generate_workload_rewards    -> trainer/workload.cpp:62-107
+//   ref_process_response             -> handlers.cpp:57-91 (the /process wire JSON)
 #include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "rollout/backend_pool.hpp"
+#include "rollout/clock.hpp"
+#include "rollout/handler.hpp"
+#include "rollout/job.hpp"
 #include "rollout/mock/policy.hpp"
 #include "rollout/trainer/harness.hpp"
 #include "rollout/trainer/workload.hpp"
@@ -123,6 +127,43 @@ int ref_generate_workload_rewards(int num_prompts, int n, uint64_t seed, double 
   return 0;
 }
 
+// Builds a Job with the given turns (assistant turns carry ids as output_ids
+// with aligned logprobs), reward and terminal status (0 DONE, 1 FAILED,
+// 2 CANCELLED), and returns build_process_response(job).dump() in out.
+// Returns the JSON length (or the needed capacity if cap is too small),
+// -1 on MalformedTurn.
+int64_t ref_process_response(const char* job_id, int n_turns, const int* roles, const int64_t* lens,
+                             const int64_t* ids, const double* lps, double reward, int status, const char* backend,
+                             char* out, int64_t cap) {
+  auto clock = std::make_shared<ManualClock>();
+  Job job(job_id, "echo", nlohmann::json::object(), SamplingParams{}, std::chrono::seconds(60), clock);
+  int64_t off = 0;
+  try {
+    for (int i = 0; i < n_turns; ++i) {
+      TokenIds v(ids + off, ids + off + lens[i]);
+      if (roles[i] == 2) {
+        job.append_turn(make_assistant_turn(std::move(v), std::vector<double>(lps + off, lps + off + lens[i])));
+      } else {
+        Turn t;
+        t.role = static_cast<Role>(roles[i]);
+        t.input_ids = std::move(v);
+        t.text = "t" + std::to_string(i);
+        job.append_turn(std::move(t));
+      }
+      off += lens[i];
+    }
+  } catch (const MalformedTurn&) {
+    return -1;
+  }
+  job.set_reward(reward);
+  if (backend && backend[0]) job.record_backend(backend);
+  clock->advance(std::chrono::milliseconds(5));
+  job.try_terminal(status == 1 ? JobStatus::FAILED : (status == 2 ? JobStatus::CANCELLED : JobStatus::DONE));
+  const std::string js = build_process_response(job).dump();
+  if ((int64_t)js.size() <= cap) std::memcpy(out, js.data(), js.size());
+  return (int64_t)js.size();
+}
+
 }  // extern "C"
 
 // ---- link stubs: httplib-backed symbols harness.cpp references but the
@@ -130,6 +171,10 @@ int ref_generate_workload_rewards(int num_prompts, int n, uint64_t seed, double 
 namespace rollout {
 namespace backend {
 std::pair<std::string, int> parse_http_address(const std::string&) { throw Error("stub", "not linked"); }
+GenerateResult BackendPool::generate(const std::string&, const TokenIds&, const SamplingParams&,
+                                     const std::function<bool()>&) {
+  throw Error("stub", "not linked");
+}
 }  // namespace backend
 namespace train {
 RolloutClient::RolloutClient(std::string, Duration) { throw Error("stub", "not linked"); }

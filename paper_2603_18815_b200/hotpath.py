@@ -222,6 +222,32 @@ def shard_lpt(load: np.ndarray, world: int) -> np.ndarray:
     return owner
 
 
+def ingest_responses(responses: list[bytes], group_off, tolerance: float = 0.0, threads: int = 0):
+    """/process response JSON (handlers.cpp:57-91 schema) -> (HostBatchArrays, n_active, n_informative)
+    via the native single-pass parser (prorl_ingest_responses)."""
+    n = len(responses)
+    bufs = (C.c_char_p * n)(*responses)
+    lens = np.array([len(r) for r in responses], dtype=np.uint64)
+    goff = np.ascontiguousarray(group_off, dtype=np.int32)
+    res = N.IngestResult()
+    check(N.lib.prorl_ingest_responses(C.cast(bufs, C.c_void_p), ptr(lens), ptr(goff), len(goff) - 1, tolerance,
+                                       threads, C.byref(res)))
+    try:
+        b = res.batch
+
+        def arr(p, n, dt):
+            if n == 0 or not p:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), shape=(n * np.dtype(dt).itemsize,)).view(
+                dt).copy()
+        out = HostBatchArrays(turns=arr(b.turns, b.n_turns, N.TURN_DTYPE), ids=arr(b.ids, b.n_tokens, np.int64),
+                              lp=arr(b.lp, b.n_tokens, np.float64), reward=arr(b.reward, b.n_rollouts, np.float64),
+                              usable=arr(b.usable, b.n_rollouts, np.uint8), group_off=goff.copy())
+        return out, res.n_active, res.n_informative
+    finally:
+        N.lib.prorl_ingest_free(C.byref(res))
+
+
 def synth_rewards(num_prompts: int, n: int, seed: int, p_informative: float = 0.5) -> np.ndarray:
     out = np.zeros(num_prompts * n, dtype=np.float64)
     check(N.lib.prorl_synth_rewards(num_prompts, n, seed, p_informative, ptr(out)))

@@ -104,6 +104,27 @@ def main() -> None:
         wl.append({"seed": seed, "num_prompts": P, "n": n, "rewards": buf.tolist()})
     out["workload"] = wl
 
+    # /process wire JSON produced by the reference's build_process_response (handlers.cpp:57-91)
+    import ctypes as C
+    resp = []
+    for case in range(24):
+        n_turns = rng.randint(0, 7)
+        roles = [rng.choice([0, 1, 2, 3]) for _ in range(n_turns)]
+        lens = [rng.randint(0, 5) for _ in range(n_turns)]
+        ids = [rng.randint(0, 151935) for _ in range(sum(lens))]
+        lps = [round(-rng.random() * 5, rng.choice([1, 3, 17])) for _ in ids]
+        status = rng.choice([0, 0, 0, 1, 2])
+        reward = rng.choice([0.0, 1.0, 0.5])
+        a = lambda x, dt: np.ascontiguousarray(x or [0], dt)
+        r_, l_, i_, p_ = a(roles, np.int32), a(lens, np.int64), a(ids, np.int64), a(lps, np.float64)
+        buf = C.create_string_buffer(1 << 16)
+        n = R.ref_process_response(f"job-{case}".encode(), n_turns, r_.ctypes.data, l_.ctypes.data, i_.ctypes.data,
+                                   p_.ctypes.data, reward, status, b"http://10.0.0.1:8000" if case % 2 else b"",
+                                   buf, len(buf))
+        resp.append({"roles": roles, "lens": lens, "ids": ids, "logprobs": lps, "reward": reward,
+                     "status": ["DONE", "FAILED", "CANCELLED"][status], "json": buf.raw[:n].decode()})
+    out["process_response"] = resp
+
     path = Path(__file__).with_name("reference_vectors.json")
     path.write_text(json.dumps(out, indent=None, separators=(",", ":")))
     print(path, path.stat().st_size)
