@@ -65,7 +65,11 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         o = BUILD / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{json_include()}", "-c", str(s), "-o", str(o)]
+            if s.suffix == ".cpp":  # host-only C++: the host compiler directly, full optimisation
+                cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{INCLUDE}",
+                       f"-I{CSRC}", f"-I{json_include()}", "-I/usr/local/cuda/include", "-c", str(s), "-o", str(o)]
+            else:
+                cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{json_include()}", "-c", str(s), "-o", str(o)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -280,8 +280,11 @@ void parse_response(const char* js, size_t n, Rollout& r) {
 
 void parse_groups(const char* const* json, const size_t* len, const int32_t* group_off, int32_t g0, int32_t g1,
                   double tol, Part& out) {
-  Rollout tmp;
   std::vector<Rollout> grp;
+  size_t bytes = 0;  // capacity estimate: a token takes >= ~5 bytes of wire JSON on average
+  for (int32_t i = group_off[g0]; i < group_off[g1]; ++i) bytes += len[i];
+  out.ids.reserve(bytes / 5);
+  out.lp.reserve(bytes / 5);
   for (int32_t g = g0; g < g1; ++g) {
     const int32_t b = group_off[g], e = group_off[g + 1];
     grp.resize((size_t)(e - b));
@@ -366,30 +369,36 @@ extern "C" int prorl_ingest_responses(const char* const* json, const size_t* len
       delete impl;
       return prorl::fail(p.status, p.error);
     }
-  size_t nt = 0, ni = 0, nr = 0;
-  for (const Part& p : parts) {
-    nt += p.turns.size();
-    ni += p.ids.size();
-    nr += p.reward.size();
+  // offsets of each part in the merged arrays, then copy the parts in parallel
+  std::vector<size_t> ot(parts.size() + 1, 0), oi(parts.size() + 1, 0), orr(parts.size() + 1, 0);
+  for (size_t t = 0; t < parts.size(); ++t) {
+    ot[t + 1] = ot[t] + parts[t].turns.size();
+    oi[t + 1] = oi[t] + parts[t].ids.size();
+    orr[t + 1] = orr[t] + parts[t].reward.size();
+    out->n_active += parts[t].n_active;
+    out->n_informative += parts[t].n_informative;
   }
-  impl->turns.reserve(nt);
-  impl->ids.reserve(ni);
-  impl->lp.reserve(ni);
-  impl->reward.reserve(nr);
-  impl->usable.reserve(nr);
-  for (const Part& p : parts) {
-    const int64_t base = (int64_t)impl->ids.size();
-    for (prorl_turn_desc d : p.turns) {
-      d.src_off += base;
-      impl->turns.push_back(d);
-    }
-    impl->ids.insert(impl->ids.end(), p.ids.begin(), p.ids.end());
-    impl->lp.insert(impl->lp.end(), p.lp.begin(), p.lp.end());
-    impl->reward.insert(impl->reward.end(), p.reward.begin(), p.reward.end());
-    impl->usable.insert(impl->usable.end(), p.usable.begin(), p.usable.end());
-    out->n_active += p.n_active;
-    out->n_informative += p.n_informative;
+  impl->turns.resize(ot.back());
+  impl->ids.resize(oi.back());
+  impl->lp.resize(oi.back());
+  impl->reward.resize(orr.back());
+  impl->usable.resize(orr.back());
+  th.clear();
+  for (size_t t = 0; t < parts.size(); ++t) {
+    th.emplace_back([&, t] {
+      const Part& p = parts[t];
+      for (size_t k = 0; k < p.turns.size(); ++k) {
+        prorl_turn_desc d = p.turns[k];
+        d.src_off += (int64_t)oi[t];
+        impl->turns[ot[t] + k] = d;
+      }
+      std::copy(p.ids.begin(), p.ids.end(), impl->ids.begin() + (ptrdiff_t)oi[t]);
+      std::copy(p.lp.begin(), p.lp.end(), impl->lp.begin() + (ptrdiff_t)oi[t]);
+      std::copy(p.reward.begin(), p.reward.end(), impl->reward.begin() + (ptrdiff_t)orr[t]);
+      std::copy(p.usable.begin(), p.usable.end(), impl->usable.begin() + (ptrdiff_t)orr[t]);
+    });
   }
+  for (auto& x : th) x.join();
   impl->group_off.assign(group_off, group_off + n_groups + 1);
   prorl_host_batch& b = out->batch;
   b.turns = impl->turns.data();
