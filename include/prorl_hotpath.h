@@ -62,13 +62,14 @@ enum { PRORL_ROLE_SYSTEM = 0, PRORL_ROLE_USER = 1, PRORL_ROLE_ASSISTANT = 2, PRO
 
 /* Number of per-turn metric buckets and the partials layout. */
 #define PRORL_TURN_BUCKETS 64
-#define PRORL_N_GLOBAL 10
+#define PRORL_N_GLOBAL 12
 #define PRORL_N_PER_TURN 5
-#define PRORL_N_PARTIALS (PRORL_N_GLOBAL + PRORL_TURN_BUCKETS * PRORL_N_PER_TURN) /* 330 */
+#define PRORL_N_PARTIALS (PRORL_N_GLOBAL + PRORL_TURN_BUCKETS * PRORL_N_PER_TURN) /* 332 */
 enum {
   PRORL_P_LOSS_SUM = 0, PRORL_P_N_ACTIVE = 1, PRORL_P_ENTROPY_SUM = 2, PRORL_P_LOGP_SUM = 3,
   PRORL_P_RATIO_SUM = 4, PRORL_P_CLIP_LO = 5, PRORL_P_CLIP_HI = 6, PRORL_P_KL1_SUM = 7,
-  PRORL_P_ADV_SUM = 8, PRORL_P_N_ROLLOUTS = 9
+  PRORL_P_ADV_SUM = 8, PRORL_P_N_ROLLOUTS = 9, PRORL_P_KL_SUM = 10 /* sum of k3 KL vs the reference policy */
+  /* 11: reserved (0) */
 };
 /* per-turn bucket k starts at PRORL_N_GLOBAL + 5*k: [N_k, loss_k, H_k, logp_k, clip_k] */
 
@@ -107,7 +108,7 @@ typedef struct prorl_loss_cfg {
   float eps_lo;       /* DAPO clip low  (default 0.2)  */
   float eps_hi;       /* DAPO clip high (default 0.28) */
   int32_t n_buckets;  /* per-turn buckets used (<= PRORL_TURN_BUCKETS) */
-  int32_t pad_;
+  float kl_coef;      /* k3 KL penalty vs the reference policy (PAPER.md:386 uses 1e-4); needs ref_lp */
 } prorl_loss_cfg;
 
 typedef struct prorl_score_cfg {
@@ -162,17 +163,20 @@ int prorl_logprob_entropy(prorl_ctx* ctx, const void* logits, int dtype, int64_t
 /* ---- K4: clipped surrogate + metrics -------------------------------------- */
 /* Adds this call's sums into partials_dev[PRORL_N_PARTIALS] (fp64) with a
  * fixed reduction order (deterministic run to run). */
+/* ref_lp (nullable): reference-policy logprob per row; with it each row adds
+ * kl_coef * k3 to its loss, k3 = exp(ref - logp) - (ref - logp) - 1, and
+ * sum(k3) to partials[PRORL_P_KL_SUM]. */
 int prorl_clipped_loss(prorl_ctx* ctx, const float* logp, const float* entropy,
                        const float* old_lp, const float* adv, const int32_t* row_seq,
-                       const int16_t* row_turn, int64_t n_rows, const prorl_loss_cfg* cfg,
-                       double* partials_dev, void* stream);
+                       const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                       const prorl_loss_cfg* cfg, double* partials_dev, void* stream);
 
 /* K2+K4 fused: one HBM pass per row and the loss epilogue in the same kernel.
  * logp/entropy outputs are optional (may be NULL). */
 int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride,
                      int32_t vocab, const int32_t* rows, const int32_t* targets,
                      const float* old_lp, const float* adv, const int32_t* row_seq,
-                     const int16_t* row_turn, int64_t n_rows, float inv_temp,
+                     const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float inv_temp,
                      const prorl_loss_cfg* cfg, float* logp, float* entropy,
                      double* partials_dev, void* stream);
 
@@ -183,10 +187,11 @@ int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_
  * the row's lse recovered as x_y inv_temp - logp_i (logp from K2). grad rows
  * are addressed like the logits rows (rows[] indirection, same row_stride,
  * same 16-B phase); grad may alias logits (in place). dtype of grad = dtype
- * of logits. dlogp (nullable) receives g_i. */
+ * of logits. dlogp (nullable) receives g_i. With ref_lp and cfg->kl_coef the
+ * k3 KL term adds kl_coef * (1 - exp(ref - logp)) / n_global to g_i. */
 int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                       const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
-                      const float* adv, const int32_t* row_seq, int64_t n_rows, float inv_temp,
+                      const float* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
                       float* dlogp, void* stream);
 

@@ -38,6 +38,7 @@ struct ScoreConfig {
   double gate_tolerance = 0.0;   // is_informative tolerance
   float inv_temperature = 1.0f;  // 1 / SamplingParams::temperature (types.hpp:59)
   int max_turn_buckets = PRORL_TURN_BUCKETS;
+  float kl_coef = 0.0f;          // k3 KL vs a reference policy (1e-4); C-ABI ref_lp path
   int vocab = 0;
   LogitsDtype dtype = LogitsDtype::BF16;
   int microbatch_rows = 16384;   // active rows per logits micro-batch
@@ -52,7 +53,7 @@ struct TurnMetrics {
 struct ScoreResult {
   double loss = 0;  // DAPO token-mean surrogate over the global batch
   std::int64_t n_active = 0;
-  double entropy = 0, logp = 0, ratio = 0, clip_lo_frac = 0, clip_hi_frac = 0, kl_k1 = 0;
+  double entropy = 0, logp = 0, ratio = 0, clip_lo_frac = 0, clip_hi_frac = 0, kl_k1 = 0, kl_k3 = 0;
   double adv_sum = 0;
   std::int64_t n_rollouts = 0;
   std::vector<TurnMetrics> per_turn;

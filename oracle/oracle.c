@@ -281,12 +281,14 @@ void oracle_logprob_entropy(const void* logits, int dtype, int64_t row_stride, i
 /* Adds one row into partials / abs_partials (|term| sums, used as the
  * condition scale of the tolerance) and counts borderline clip decisions. */
 static void loss_row(double logp, double ent, double old, double A, int turn, double lo, double hi, int n_buckets,
-                     double* P, double* Q, int64_t* n_border) {
+                     const double* ref, double kl_coef, double* P, double* Q, int64_t* n_border) {
   const double ratio = exp(logp - old);
   const double pg1 = ratio * A;
   const double cr = ratio < lo ? lo : (ratio > hi ? hi : ratio);
   const double pg2 = cr * A;
-  const double loss = -(pg1 < pg2 ? pg1 : pg2);
+  /* k3 KL vs the reference policy (coefficient 1e-4) */
+  const double kl = ref ? expm1(*ref - logp) - (*ref - logp) : 0.0;
+  const double loss = -(pg1 < pg2 ? pg1 : pg2) + kl_coef * kl;
   const double clo = (ratio < lo && A < 0) ? 1.0 : 0.0;
   const double chi = (ratio > hi && A > 0) ? 1.0 : 0.0;
   if (n_border && (fabs(ratio - lo) <= 1e-5 * lo || fabs(ratio - hi) <= 1e-5 * hi)) ++*n_border;
@@ -295,6 +297,8 @@ static void loss_row(double logp, double ent, double old, double A, int turn, do
     P[k] += g[k];
     if (Q) Q[k] += fabs(g[k]);
   }
+  P[PRORL_P_KL_SUM] += kl;
+  if (Q) Q[PRORL_P_KL_SUM] += fabs(kl);
   int b = turn < 0 ? 0 : (turn >= n_buckets ? n_buckets - 1 : turn);
   const double bv[5] = {1.0, loss, ent, logp, clo + chi};
   for (int k = 0; k < 5; ++k) {
@@ -304,12 +308,14 @@ static void loss_row(double logp, double ent, double old, double A, int turn, do
 }
 
 void oracle_loss(const double* logp, const double* ent, const float* old_lp, const double* adv, const int32_t* row_seq,
-                 const int16_t* row_turn, int64_t n_rows, float eps_lo, float eps_hi, int n_buckets, double* partials,
-                 double* abs_partials, int64_t* n_border) {
+                 const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float eps_lo, float eps_hi, float kl_coef,
+                 int n_buckets, double* partials, double* abs_partials, int64_t* n_border) {
   const double lo = 1.0 - (double)eps_lo, hi = 1.0 + (double)eps_hi;
-  for (int64_t i = 0; i < n_rows; ++i)
-    loss_row(logp[i], ent[i], (double)old_lp[i], adv[row_seq[i]], row_turn[i], lo, hi, n_buckets, partials,
-             abs_partials, n_border);
+  for (int64_t i = 0; i < n_rows; ++i) {
+    const double ref = ref_lp ? (double)ref_lp[i] : 0.0;
+    loss_row(logp[i], ent[i], (double)old_lp[i], adv[row_seq[i]], row_turn[i], lo, hi, n_buckets,
+             ref_lp ? &ref : NULL, (double)kl_coef, partials, abs_partials, n_border);
+  }
 }
 
 /* ---- K5: backward through the log-softmax (SURVEY §8 f rank 1) ------------------------ */
@@ -319,8 +325,8 @@ void oracle_loss(const double* logp, const double* ent, const float* old_lp, con
  * border[i] = 1 when the clip decision is within 1e-5 of flipping. */
 void oracle_logits_grad(const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
                         const int32_t* targets, const float* old_lp, const double* adv, const int32_t* row_seq,
-                        int64_t n_rows, float inv_temp, float eps_lo, float eps_hi, double n_global, double* grad,
-                        double* dlogp, uint8_t* border) {
+                        const float* ref_lp, int64_t n_rows, float inv_temp, float eps_lo, float eps_hi,
+                        float kl_coef, double n_global, double* grad, double* dlogp, uint8_t* border) {
   const size_t es = dtype == PRORL_BF16 ? 2 : 4;
   const double it = (double)inv_temp, lo = 1.0 - (double)eps_lo, hi = 1.0 + (double)eps_hi;
   for (int64_t i = 0; i < n_rows; ++i) {
@@ -332,7 +338,8 @@ void oracle_logits_grad(const void* logits, int dtype, int64_t row_stride, int32
     const double A = adv[row_seq[i]];
     const double ratio = exp(lp - (double)old_lp[i]);
     const double pg1 = ratio * A, pg2 = (ratio < lo ? lo : (ratio > hi ? hi : ratio)) * A;
-    const double g = pg1 <= pg2 ? -A * ratio / n_global : 0.0;
+    double g = pg1 <= pg2 ? -A * ratio / n_global : 0.0;
+    if (ref_lp) g += (double)kl_coef * (1.0 - exp((double)ref_lp[i] - lp)) / n_global;
     if (dlogp) dlogp[i] = g;
     if (border) border[i] = (fabs(ratio - lo) <= 1e-5 * lo || fabs(ratio - hi) <= 1e-5 * hi) ? 1 : 0;
     double* gr = grad + (size_t)i * vocab;
@@ -385,7 +392,7 @@ static void* score_worker(void* arg) {
     double lp, ent;
     oracle_row_logprob(row, cfg->dtype, cfg->vocab, w->pk->act_target[i], cfg->inv_temperature, &lp, &ent);
     loss_row(lp, ent, (double)w->pk->act_old_lp[i], w->adv[w->pk->act_seq[i]], w->pk->act_turn[i], lo, hi,
-             cfg->loss.n_buckets, w->P, w->Q, &w->n_border);
+             cfg->loss.n_buckets, NULL, 0.0, w->P, w->Q, &w->n_border);
     if (w->out_logp) w->out_logp[i] = lp;
     if (w->out_ent) w->out_ent[i] = ent;
     w->gen_s += t1 - t0;

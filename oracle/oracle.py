@@ -16,7 +16,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libref.so"
-N_PARTIALS = 330
+N_PARTIALS = 332
 
 vp = C.c_void_p
 i32, i64, u64, f32, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
@@ -35,7 +35,7 @@ class OraclePacked(C.Structure):
 
 
 class LossCfg(C.Structure):  # layout of prorl_loss_cfg (include/prorl_hotpath.h)
-    _fields_ = [("eps_lo", f32), ("eps_hi", f32), ("n_buckets", i32), ("pad_", i32)]
+    _fields_ = [("eps_lo", f32), ("eps_hi", f32), ("n_buckets", i32), ("kl_coef", f32)]
 
 
 class ScoreCfg(C.Structure):  # layout of prorl_score_cfg
@@ -86,10 +86,10 @@ def lib() -> C.CDLL:
             "oracle_gen_logits": (None, [vp, C.c_int, i64, i32, i64, i64, vp, vp, u64, f32]),
             "oracle_row_logprob": (None, [vp, C.c_int, i32, i32, f32, vp, vp]),
             "oracle_logprob_entropy": (None, [vp, C.c_int, i64, i32, vp, vp, i64, f32, vp, vp]),
-            "oracle_loss": (None, [vp, vp, vp, vp, vp, vp, i64, f32, f32, C.c_int, vp, vp, vp]),
+            "oracle_loss": (None, [vp, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, C.c_int, vp, vp, vp]),
             "oracle_score_batch": (C.c_int, [vp, vp, u64, f32, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
-            "oracle_logits_grad": (None, [vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, i64, f32, f32, f32, f64, vp, vp,
-                                          vp]),
+            "oracle_logits_grad": (None, [vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f64,
+                                          vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -179,18 +179,20 @@ def logprob_entropy(logits: np.ndarray, targets, rows=None, inv_temp=1.0, vocab=
     return lp, ent
 
 
-def loss(logp, ent, old_lp, adv, row_seq, row_turn, eps_lo=0.2, eps_hi=0.28, n_buckets=64):
+def loss(logp, ent, old_lp, adv, row_seq, row_turn, eps_lo=0.2, eps_hi=0.28, n_buckets=64, ref_lp=None,
+         kl_coef=0.0):
     P, Q = np.zeros(N_PARTIALS), np.zeros(N_PARTIALS)
     nb = C.c_int64(0)
     lib().oracle_loss(_p(np.ascontiguousarray(logp, np.float64)), _p(np.ascontiguousarray(ent, np.float64)),
                       _p(np.ascontiguousarray(old_lp, np.float32)), _p(np.ascontiguousarray(adv, np.float64)),
                       _p(np.ascontiguousarray(row_seq, np.int32)), _p(np.ascontiguousarray(row_turn, np.int16)),
-                      len(logp), eps_lo, eps_hi, n_buckets, _p(P), _p(Q), C.byref(nb))
+                      _p(None if ref_lp is None else np.ascontiguousarray(ref_lp, np.float32)),
+                      len(logp), eps_lo, eps_hi, kl_coef, n_buckets, _p(P), _p(Q), C.byref(nb))
     return P, Q, nb.value
 
 
 def logits_grad(logits: np.ndarray, targets, old_lp, adv, row_seq, n_global, rows=None, inv_temp=1.0, eps_lo=0.2,
-                eps_hi=0.28, vocab=None):
+                eps_hi=0.28, vocab=None, ref_lp=None, kl_coef=0.0):
     """Oracle dL/dlogits (fp64) [n_rows x V], dL/dlogp [n_rows], border flags [n_rows]."""
     dtype = 0 if logits.dtype == np.uint16 else 1
     V = vocab or logits.shape[1]
@@ -202,8 +204,9 @@ def logits_grad(logits: np.ndarray, targets, old_lp, adv, row_seq, n_global, row
     r = None if rows is None else np.ascontiguousarray(rows, np.int32)
     lib().oracle_logits_grad(_p(logits), dtype, logits.shape[1], V, _p(r), _p(t),
                              _p(np.ascontiguousarray(old_lp, np.float32)), _p(np.ascontiguousarray(adv, np.float64)),
-                             _p(np.ascontiguousarray(row_seq, np.int32)), n, inv_temp, eps_lo, eps_hi, n_global, _p(g),
-                             _p(dl), _p(bd))
+                             _p(np.ascontiguousarray(row_seq, np.int32)),
+                             _p(None if ref_lp is None else np.ascontiguousarray(ref_lp, np.float32)), n, inv_temp,
+                             eps_lo, eps_hi, kl_coef, n_global, _p(g), _p(dl), _p(bd))
     return g, dl, bd
 
 

@@ -17,10 +17,10 @@ LIB_PATH = Path(__file__).resolve().parent / "libprorl_hotpath.so"
 
 PRORL_BF16, PRORL_FP32 = 0, 1
 ROLE_SYSTEM, ROLE_USER, ROLE_ASSISTANT, ROLE_TOOL = 0, 1, 2, 3
-TURN_BUCKETS, N_GLOBAL, N_PER_TURN = 64, 10, 5
+TURN_BUCKETS, N_GLOBAL, N_PER_TURN = 64, 12, 5
 N_PARTIALS = N_GLOBAL + TURN_BUCKETS * N_PER_TURN
 (P_LOSS_SUM, P_N_ACTIVE, P_ENTROPY_SUM, P_LOGP_SUM, P_RATIO_SUM, P_CLIP_LO, P_CLIP_HI,
- P_KL1_SUM, P_ADV_SUM, P_N_ROLLOUTS) = range(10)
+ P_KL1_SUM, P_ADV_SUM, P_N_ROLLOUTS, P_KL_SUM) = range(11)
 
 # Turn descriptor: must match prorl_turn_desc (24 bytes).
 TURN_DTYPE = np.dtype([("src_off", "<i8"), ("traj", "<i4"), ("len", "<i4"), ("role", "u1"), ("pad", "u1", (7,))])
@@ -44,7 +44,7 @@ class Packed(C.Structure):
 
 
 class LossCfg(C.Structure):
-    _fields_ = [("eps_lo", C.c_float), ("eps_hi", C.c_float), ("n_buckets", C.c_int32), ("pad_", C.c_int32)]
+    _fields_ = [("eps_lo", C.c_float), ("eps_hi", C.c_float), ("n_buckets", C.c_int32), ("kl_coef", C.c_float)]
 
 
 class ScoreCfg(C.Structure):
@@ -86,10 +86,10 @@ def _load() -> C.CDLL:
         "prorl_pack": (C.c_int, [vp, vp, i64, vp, vp, i64, i32, i32, C.POINTER(Packed), vp]),
         "prorl_grpo_adv": (C.c_int, [vp, vp, vp, vp, i32, i32, f32, f64, vp, vp, vp, vp]),
         "prorl_logprob_entropy": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, i64, f32, vp, vp, vp]),
-        "prorl_clipped_loss": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(LossCfg), vp, vp]),
-        "prorl_score_rows": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32,
+        "prorl_clipped_loss": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(LossCfg), vp, vp]),
+        "prorl_score_rows": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, vp, i64, f32,
                                        C.POINTER(LossCfg), vp, vp, vp, vp]),
-        "prorl_logits_grad": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32,
+        "prorl_logits_grad": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, vp, i64, f32,
                                         C.POINTER(LossCfg), f64, vp, i64, vp, vp]),
         "prorl_ingest_responses": (C.c_int, [vp, vp, vp, i32, f64, i32, C.POINTER(IngestResult)]),
         "prorl_ingest_free": (C.c_int, [C.POINTER(IngestResult)]),

@@ -195,46 +195,47 @@ int prorl_logprob_entropy(prorl_ctx* c, const void* logits, int dtype, int64_t r
                           float* entropy, void* stream) {
   if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_logprob_entropy: null ctx");
   PRORL_CUDA(cudaSetDevice(c->device));
-  return launch_score(c, logits, dtype, row_stride, vocab, rows, targets, nullptr, nullptr, nullptr, nullptr, n_rows,
-                      inv_temp, nullptr, logp, entropy, nullptr, 0, false, nullptr, S(stream));
+  return launch_score(c, logits, dtype, row_stride, vocab, rows, targets, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      n_rows, inv_temp, nullptr, logp, entropy, nullptr, 0, false, nullptr, S(stream));
 }
 
 int prorl_clipped_loss(prorl_ctx* c, const float* logp, const float* entropy, const float* old_lp, const float* adv,
-                       const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, const prorl_loss_cfg* cfg,
-                       double* partials_dev, void* stream) {
+                       const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                       const prorl_loss_cfg* cfg, double* partials_dev, void* stream) {
   if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_clipped_loss: null ctx/cfg");
   PRORL_CUDA(cudaSetDevice(c->device));
   const int rows = loss_slab_rows(c);
   PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(rows, score_slab_rows(c))));
   int used = 0;
-  PRORL_TRY(launch_loss(c, logp, entropy, old_lp, adv, row_seq, row_turn, n_rows, cfg, c->slab.as<double>(), rows,
-                        &used, S(stream)));
+  PRORL_TRY(launch_loss(c, logp, entropy, old_lp, adv, row_seq, row_turn, ref_lp, n_rows, cfg, c->slab.as<double>(),
+                        rows, &used, S(stream)));
   return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
 }
 
 int prorl_score_rows(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                      const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
-                     const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, float inv_temp,
-                     const prorl_loss_cfg* cfg, float* logp, float* entropy, double* partials_dev, void* stream) {
+                     const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                     float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* partials_dev,
+                     void* stream) {
   if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_rows: null ctx/cfg");
   PRORL_CUDA(cudaSetDevice(c->device));
   const int srows = score_slab_rows(c);
   PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(srows, loss_slab_rows(c))));
   int used = 0;
-  PRORL_TRY(launch_score(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, n_rows,
-                         inv_temp, cfg, logp, entropy, c->slab.as<double>(), srows, false, &used, S(stream)));
+  PRORL_TRY(launch_score(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, ref_lp,
+                         n_rows, inv_temp, cfg, logp, entropy, c->slab.as<double>(), srows, false, &used, S(stream)));
   return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
 }
 
 int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                       const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
-                      const float* adv, const int32_t* row_seq, int64_t n_rows, float inv_temp,
+                      const float* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride, float* dlogp,
                       void* stream) {
   if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_logits_grad: null ctx/cfg");
   PRORL_CUDA(cudaSetDevice(c->device));
-  return launch_grad(c, logits, dtype, row_stride, vocab, rows, targets, logp, old_lp, adv, row_seq, n_rows, inv_temp,
-                     cfg, n_global, grad, grad_stride, dlogp, S(stream));
+  return launch_grad(c, logits, dtype, row_stride, vocab, rows, targets, logp, old_lp, adv, row_seq, ref_lp, n_rows,
+                     inv_temp, cfg, n_global, grad, grad_stride, dlogp, S(stream));
 }
 
 int prorl_nccl_unique_id(uint8_t* id128) {
@@ -431,7 +432,7 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
       buf = b;
     }
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
-                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, n,
+                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
   }
   PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));

@@ -84,15 +84,17 @@ int launch_grpo(prorl_ctx* ctx, const double* reward, const uint8_t* usable, con
 // existing slab content). Returns the number of slab rows used via *slab_rows.
 int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                  const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
-                 const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, float inv_temp,
-                 const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
+                 const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                 float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
                  bool accumulate, int* rows_used, cudaStream_t st);
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp,
-                const float* adv, const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows,
-                const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used, cudaStream_t st);
+                const float* adv, const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp,
+                int64_t n_rows, const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used,
+                cudaStream_t st);
 int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
                 const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
-                const int32_t* row_seq, int64_t n_rows, float inv_temp, const prorl_loss_cfg* cfg, double n_global,
+                const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
+                const prorl_loss_cfg* cfg, double n_global,
                 void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st);
 int launch_slab_reduce(const double* slab, int slab_rows, double* partials, cudaStream_t st);
 int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,

@@ -36,6 +36,8 @@ struct GradArgs {
   const float* old_lp;
   const float* adv;
   const int32_t* row_seq;
+  const float* ref_lp;  // nullable (k3 KL term)
+  float kl_coef;
   int64_t n_rows;
   float c;         // inv_temp * log2 e
   float inv_temp;
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
       const float A = p.adv[p.row_seq[i]];
       const float ratio = expf(lp - old);
       const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
-      const float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
+      float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
+      if (p.ref_lp) dl = fmaf(p.kl_coef * p.inv_n, -expm1f(p.ref_lp[i] - lp), dl);  // d(k3)/dlogp = 1 - e^(ref-lp)
       if (p.dlogp) p.dlogp[i] = dl;
       s = -dl * p.inv_temp;  // grad_v = s * p_v for v != y, grad_y = -s * (1 - p_y)
       l2 = fmaf(xy, p.c, -lp * kLog2e);                            // lse in base-2 units
@@ -173,8 +176,9 @@ int run_grad(const GradArgs& a, int n_sm, cudaStream_t st) {
 
 int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
                 const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
-                const int32_t* row_seq, int64_t n_rows, float inv_temp, const prorl_loss_cfg* cfg, double n_global,
-                void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st) {
+                const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
+                const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride, float* dlogp,
+                cudaStream_t st) {
   if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "logits_grad: unknown dtype");
   if (vocab <= 0 || row_stride < vocab) return fail(PRORL_E_SHAPE, "logits_grad: need vocab > 0, row_stride >= vocab");
   if (grad_stride != row_stride)
@@ -196,6 +200,8 @@ int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_strid
   a.old_lp = old_lp;
   a.adv = adv;
   a.row_seq = row_seq;
+  a.ref_lp = ref_lp;
+  a.kl_coef = cfg->kl_coef;
   a.n_rows = n_rows;
   a.c = inv_temp * kLog2e;
   a.inv_temp = inv_temp;

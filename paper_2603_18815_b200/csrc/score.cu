@@ -235,6 +235,8 @@ struct ScoreArgs {
   const float* adv;
   const int32_t* row_seq;
   const int16_t* row_turn;
+  const float* ref_lp;  // nullable
+  float kl_coef;
   float lo_bound, hi_bound;  // 1 - eps_lo, 1 + eps_hi
   int n_buckets;
   float* logp;
@@ -243,11 +245,18 @@ struct ScoreArgs {
   int accumulate;
 };
 
-// Per-row loss terms (App. B.4/B.5), fp32 math.
+// k3 KL estimator e^d - d - 1 (d = ref - logp), accurate for small |d|.
+__device__ __forceinline__ float kl_k3(float d) {
+  if (fabsf(d) < 0.125f) return d * d * fmaf(d, fmaf(d, fmaf(d, 1.f / 120.f, 1.f / 24.f), 1.f / 6.f), 0.5f);
+  return expm1f(d) - d;
+}
+
+// Per-row loss terms (App. B.4/B.5 + optional KL), fp32 math.
 struct RowLoss {
-  float loss, ratio, clip_lo, clip_hi;
+  float loss, ratio, clip_lo, clip_hi, kl;
 };
-__device__ __forceinline__ RowLoss row_loss(float logp, float old, float A, float lo, float hi) {
+__device__ __forceinline__ RowLoss row_loss(float logp, float old, float A, float lo, float hi, const float* ref,
+                                            int64_t i, float kl_coef) {
   RowLoss r;
   r.ratio = expf(logp - old);
   const float pg1 = r.ratio * A;
@@ -255,10 +264,17 @@ __device__ __forceinline__ RowLoss row_loss(float logp, float old, float A, floa
   r.loss = -fminf(pg1, pg2);
   r.clip_lo = (r.ratio < lo && A < 0.f) ? 1.f : 0.f;
   r.clip_hi = (r.ratio > hi && A > 0.f) ? 1.f : 0.f;
+  r.kl = 0.f;
+  if (ref) {
+    r.kl = kl_k3(ref[i] - logp);
+    r.loss = fmaf(kl_coef, r.kl, r.loss);
+  }
   return r;
 }
 
-constexpr int kNG = 8;  // per-row global sums kept by the loss epilogue
+// per-row global sums kept by the loss epilogue; index = partials index
+// (8, 9 belong to K3 and stay 0 here; 10 = sum k3 KL)
+constexpr int kNG = 11;
 constexpr int kBucketDoubles = PRORL_TURN_BUCKETS * PRORL_N_PER_TURN;
 
 // Block-level merge of per-warp partials (fixed warp order) into slab row b.
@@ -390,7 +406,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         const float A = p.adv[p.row_seq[i]];
         int k = p.row_turn[i];
         k = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
-        const RowLoss rl = row_loss(logp, old, A, p.lo_bound, p.hi_bound);
+        const RowLoss rl = row_loss(logp, old, A, p.lo_bound, p.hi_bound, p.ref_lp, i, p.kl_coef);
         g[0] += rl.loss;
         g[1] += 1.0;
         g[2] += ent;
@@ -399,6 +415,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         g[5] += rl.clip_lo;
         g[6] += rl.clip_hi;
         g[7] += (double)(old - logp);
+        g[10] += rl.kl;
         double* bk = bk_w + warp * kBucketDoubles + k * PRORL_N_PER_TURN;
         bk[0] += 1.0;
         bk[1] += rl.loss;
@@ -425,7 +442,8 @@ constexpr int kLossWarps = 8;
 __global__ void __launch_bounds__(kLossWarps * 32)
     k_loss(const float* __restrict__ logp, const float* __restrict__ entropy, const float* __restrict__ old_lp,
            const float* __restrict__ adv, const int32_t* __restrict__ row_seq, const int16_t* __restrict__ row_turn,
-           int64_t n_rows, float lo, float hi, int n_buckets, double* slab) {
+           const float* __restrict__ ref_lp, float kl_coef, int64_t n_rows, float lo, float hi, int n_buckets,
+           double* slab) {
   __shared__ double g_w[kLossWarps * kNG];
   __shared__ double bk_w[kLossWarps * kBucketDoubles];
   __shared__ int s_key[kLossWarps][32];
@@ -446,7 +464,7 @@ __global__ void __launch_bounds__(kLossWarps * 32)
       const float A = adv[row_seq[i]];
       int k = row_turn[i];
       key = k < 0 ? 0 : (k >= n_buckets ? n_buckets - 1 : k);
-      const RowLoss r = row_loss(lp, old, A, lo, hi);
+      const RowLoss r = row_loss(lp, old, A, lo, hi, ref_lp, i, kl_coef);
       g[0] += r.loss;
       g[1] += 1.0;
       g[2] += ent;
@@ -455,6 +473,7 @@ __global__ void __launch_bounds__(kLossWarps * 32)
       g[5] += r.clip_lo;
       g[6] += r.clip_hi;
       g[7] += (double)(old - lp);
+      g[10] += r.kl;
       s_val[warp][lane][0] = 1.f;
       s_val[warp][lane][1] = r.loss;
       s_val[warp][lane][2] = ent;
@@ -547,8 +566,8 @@ int loss_slab_rows(prorl_ctx* ctx) { return 2 * ctx->n_sm; }
 
 int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                  const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
-                 const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, float inv_temp,
-                 const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
+                 const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                 float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
                  bool accumulate, int* rows_used, cudaStream_t st) {
   if (rows_used) *rows_used = 0;
   if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "score: unknown logits dtype");
@@ -571,6 +590,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.adv = adv;
   a.row_seq = row_seq;
   a.row_turn = row_turn;
+  a.ref_lp = ref_lp;
   a.logp = logp;
   a.entropy = entropy;
   a.slab = slab;
@@ -579,6 +599,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
     a.lo_bound = 1.0f - cfg->eps_lo;
     a.hi_bound = 1.0f + cfg->eps_hi;
     a.n_buckets = cfg->n_buckets;
+    a.kl_coef = cfg->kl_coef;
   }
   if (dtype == PRORL_BF16)
     return cfg ? run_score<__nv_bfloat16, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st)
@@ -588,8 +609,8 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
 }
 
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp, const float* adv,
-                const int32_t* row_seq, const int16_t* row_turn, int64_t n_rows, const prorl_loss_cfg* cfg,
-                double* slab, int slab_rows, int* rows_used, cudaStream_t st) {
+                const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used, cudaStream_t st) {
   *rows_used = 0;
   if (cfg->n_buckets < 1 || cfg->n_buckets > PRORL_TURN_BUCKETS)
     return fail(PRORL_E_SHAPE, "loss: n_buckets out of [1, 64]");
@@ -597,8 +618,8 @@ int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const f
   const int64_t tiles = (n_rows + 31) / 32;
   int grid = (int)std::min<int64_t>((int64_t)slab_rows, (tiles + kLossWarps - 1) / kLossWarps);
   (void)ctx;
-  k_loss<<<grid, kLossWarps * 32, 0, st>>>(logp, entropy, old_lp, adv, row_seq, row_turn, n_rows,
-                                           1.0f - cfg->eps_lo, 1.0f + cfg->eps_hi, cfg->n_buckets, slab);
+  k_loss<<<grid, kLossWarps * 32, 0, st>>>(logp, entropy, old_lp, adv, row_seq, row_turn, ref_lp, cfg->kl_coef,
+                                           n_rows, 1.0f - cfg->eps_lo, 1.0f + cfg->eps_hi, cfg->n_buckets, slab);
   PRORL_CUDA(cudaGetLastError());
   *rows_used = grid;
   return PRORL_OK;

@@ -105,6 +105,7 @@ ScoreResult finalize(const double* p, int n_buckets) {
   r.clip_lo_frac = p[PRORL_P_CLIP_LO] / n;
   r.clip_hi_frac = p[PRORL_P_CLIP_HI] / n;
   r.kl_k1 = p[PRORL_P_KL1_SUM] / n;
+  r.kl_k3 = p[PRORL_P_KL_SUM] / n;
   r.adv_sum = p[PRORL_P_ADV_SUM];
   r.n_rollouts = (std::int64_t)p[PRORL_P_N_ROLLOUTS];
   for (int k = 0; k < n_buckets && k < PRORL_TURN_BUCKETS; ++k) {
@@ -191,6 +192,7 @@ ScoreResult DeviceScorer::score_batch(const HostBatch& batch, LogitsSource& logi
   c.loss.eps_lo = cfg.eps_lo;
   c.loss.eps_hi = cfg.eps_hi;
   c.loss.n_buckets = cfg.max_turn_buckets;
+  c.loss.kl_coef = cfg.kl_coef;
   c.inv_temperature = cfg.inv_temperature;
   c.adv_eps = cfg.adv_eps;
   c.ddof = cfg.ddof;

@@ -29,9 +29,10 @@ class LossConfig:
     eps_lo: float = 0.2
     eps_hi: float = 0.28
     n_buckets: int = N.TURN_BUCKETS
+    kl_coef: float = 0.0  # k3 KL vs the reference policy (1e-4); needs ref_lp
 
     def c(self) -> N.LossCfg:
-        return N.LossCfg(self.eps_lo, self.eps_hi, self.n_buckets, 0)
+        return N.LossCfg(self.eps_lo, self.eps_hi, self.n_buckets, self.kl_coef)
 
 
 @dataclass
@@ -122,18 +123,19 @@ class Scorer:
 
     # ---- K4 ----
     def clipped_loss(self, logp, entropy, old_lp, adv, row_seq, row_turn, cfg: LossConfig | None = None,
-                     partials: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                     partials: torch.Tensor | None = None, ref_lp=None, stream=None) -> torch.Tensor:
         if partials is None:
             partials = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=logp.device)
         c = (cfg or LossConfig()).c()
         check(N.lib.prorl_clipped_loss(self.ctx, ptr(logp), ptr(entropy), ptr(old_lp), ptr(adv), ptr(row_seq),
-                                       ptr(row_turn), logp.numel(), C.byref(c), ptr(partials), _stream(stream)))
+                                       ptr(row_turn), ptr(ref_lp), logp.numel(), C.byref(c), ptr(partials),
+                                       _stream(stream)))
         return partials
 
     # ---- K2+K4 fused ----
     def score_rows(self, logits, targets, old_lp, adv, row_seq, row_turn, rows=None, inv_temp: float = 1.0,
                    cfg: LossConfig | None = None, partials=None, want_rows: bool = True, vocab: int | None = None,
-                   stream=None):
+                   ref_lp=None, stream=None):
         n = targets.numel()
         dev = targets.device
         if partials is None:
@@ -143,14 +145,14 @@ class Scorer:
         c = (cfg or LossConfig()).c()
         V = vocab if vocab is not None else logits.shape[1]
         check(N.lib.prorl_score_rows(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
-                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), n, inv_temp,
-                                     C.byref(c), ptr(logp), ptr(ent), ptr(partials), _stream(stream)))
+                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
+                                     inv_temp, C.byref(c), ptr(logp), ptr(ent), ptr(partials), _stream(stream)))
         return partials, logp, ent
 
     # ---- K5: backward through the log-softmax ----
     def logits_grad(self, logits, targets, logp, old_lp, adv, row_seq, n_global: float, rows=None,
                     inv_temp: float = 1.0, cfg: LossConfig | None = None, grad=None, vocab: int | None = None,
-                    want_dlogp: bool = False, stream=None):
+                    want_dlogp: bool = False, ref_lp=None, stream=None):
         """dL/dlogits (same dtype/layout as logits; grad=logits for in place)."""
         if grad is None:
             grad = torch.empty_like(logits)
@@ -159,7 +161,8 @@ class Scorer:
         c = (cfg or LossConfig()).c()
         V = vocab if vocab is not None else logits.shape[1]
         check(N.lib.prorl_logits_grad(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
-                                      ptr(targets), ptr(logp), ptr(old_lp), ptr(adv), ptr(row_seq), n, inv_temp,
+                                      ptr(targets), ptr(logp), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(ref_lp), n,
+                                      inv_temp,
                                       C.byref(c), float(n_global), ptr(grad), grad.stride(0), ptr(dl),
                                       _stream(stream)))
         return grad, dl
@@ -302,7 +305,8 @@ def finalize(p: np.ndarray) -> dict:
     out = {
         "loss": p[N.P_LOSS_SUM] / n, "n_active": int(p[N.P_N_ACTIVE]), "entropy": p[N.P_ENTROPY_SUM] / n,
         "logp": p[N.P_LOGP_SUM] / n, "ratio": p[N.P_RATIO_SUM] / n, "clip_lo_frac": p[N.P_CLIP_LO] / n,
-        "clip_hi_frac": p[N.P_CLIP_HI] / n, "kl_k1": p[N.P_KL1_SUM] / n, "adv_sum": p[N.P_ADV_SUM],
+        "clip_hi_frac": p[N.P_CLIP_HI] / n, "kl_k1": p[N.P_KL1_SUM] / n, "kl_k3": p[N.P_KL_SUM] / n,
+        "adv_sum": p[N.P_ADV_SUM],
         "n_rollouts": int(p[N.P_N_ROLLOUTS]),
     }
     per_turn = p[N.N_GLOBAL:].reshape(N.TURN_BUCKETS, N.N_PER_TURN)

@@ -88,6 +88,24 @@ def test_logits_grad_padded_stride_rows_inplace(scorer, cuda):
     assert torch.equal(g_out[:, :V], ref_x[:, :V])
 
 
+def test_logits_grad_with_kl(scorer, cuda):
+    from paper_2603_18815_b200.hotpath import LossConfig
+    V, n = 4099, 64
+    x, host, t, old, adv, seq = _case(scorer, cuda, V, n, "bf16", seed=21)
+    td = dev(t, cuda)
+    lp, _ = scorer.logprob_entropy(x, td)
+    ref = (lp.cpu().numpy() + np.random.default_rng(3).normal(0, 0.4, n)).astype(np.float32)
+    cfg = LossConfig(kl_coef=0.25)
+    g, dl = scorer.logits_grad(x, td, lp, dev(old, cuda), dev(adv, cuda), dev(seq, cuda), 300.0, cfg=cfg,
+                               ref_lp=dev(ref, cuda), want_dlogp=True)
+    og, odl, bd = O.logits_grad(host, t, old, adv.astype(np.float64), seq, 300.0, ref_lp=ref, kl_coef=0.25)
+    ok = bd == 0
+    d = dl.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(d[ok] - odl[ok]) <= 1e-5 * np.abs(odl[ok]) + 1e-10)
+    got = g.float().cpu().numpy().astype(np.float64)
+    assert not ((np.abs(got - og) > 2.0 ** -8 * np.abs(og) + 1e-30) & ok[:, None]).any()
+
+
 def test_logits_grad_layout_errors(scorer, cuda):
     from paper_2603_18815_b200.hotpath import RolloutError
     x = torch.zeros((4, 64), dtype=torch.bfloat16, device=cuda)

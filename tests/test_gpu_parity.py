@@ -295,6 +295,22 @@ def test_clipped_loss_vs_oracle(scorer, cuda, n):
     assert_partials_close(p.cpu().numpy(), P, Q, nb, "loss")
 
 
+@pytest.mark.parametrize("kl_coef", [1e-4, 0.5])
+def test_clipped_loss_with_kl_vs_oracle(scorer, cuda, kl_coef):
+    """k3 KL penalty vs a reference policy (coefficient 1e-4)."""
+    from paper_2603_18815_b200.hotpath import LossConfig
+    rng = np.random.default_rng(17)
+    logp, ent, old, adv, seq, turn = _loss_inputs(20000, rng)
+    ref = (logp + rng.normal(0, 0.3, len(logp)) * (rng.random(len(logp)) < 0.9)).astype(np.float32)
+    cfg = LossConfig(kl_coef=kl_coef)
+    p = scorer.clipped_loss(dev(logp, cuda), dev(ent, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
+                            dev(turn, cuda), cfg=cfg, ref_lp=dev(ref, cuda))
+    P, Q, nb = O.loss(logp.astype(np.float64), ent.astype(np.float64), old, adv.astype(np.float64), seq, turn,
+                      ref_lp=ref, kl_coef=kl_coef)
+    assert P[N.P_KL_SUM] > 0
+    assert_partials_close(p.cpu().numpy(), P, Q, nb, "loss+kl")
+
+
 def test_clipped_loss_deterministic(scorer, cuda):
     rng = np.random.default_rng(9)
     args = [dev(a, cuda) for a in _loss_inputs(50000, rng)]
