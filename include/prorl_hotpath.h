@@ -195,6 +195,16 @@ int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
                       float* dlogp, void* stream);
 
+/* ---- K6: fused LM head + logprob / entropy (SURVEY §8 f rank 2) ------------- */
+/* logits_i = W . h_i (bf16 hidden [n_rows x d], row stride h_stride; bf16
+ * LM-head weight [V x d], row stride w_stride; d % 64 == 0, 16-B aligned
+ * rows) computed on tcgen05 tensor cores tile by tile and reduced in place:
+ * logp_i = log softmax(logits_i * inv_temp)[targets_i], entropy_i as K2.
+ * The logits are never materialised in HBM. */
+int prorl_lmhead_logprob(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const void* weight,
+                         int64_t w_stride, int32_t d, int32_t vocab, const int32_t* targets,
+                         int64_t n_rows, float inv_temp, float* logp, float* entropy, void* stream);
+
 /* ---- NCCL ------------------------------------------------------------------ */
 /* 128-byte ncclUniqueId produced on rank 0, broadcast by the caller. */
 int prorl_nccl_unique_id(uint8_t* id128);

@@ -238,6 +238,15 @@ int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_s
                      inv_temp, cfg, n_global, grad, grad_stride, dlogp, S(stream));
 }
 
+int prorl_lmhead_logprob(prorl_ctx* c, const void* hidden, int64_t h_stride, const void* weight, int64_t w_stride,
+                         int32_t d, int32_t vocab, const int32_t* targets, int64_t n_rows, float inv_temp,
+                         float* logp, float* entropy, void* stream) {
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_lmhead_logprob: null ctx");
+  PRORL_CUDA(cudaSetDevice(c->device));
+  return launch_lmhead(c, hidden, h_stride, weight, w_stride, d, vocab, targets, n_rows, inv_temp, logp, entropy,
+                       S(stream));
+}
+
 int prorl_nccl_unique_id(uint8_t* id128) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   PRORL_NCCL_API();

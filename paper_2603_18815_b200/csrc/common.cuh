@@ -19,6 +19,12 @@ void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 
+#define PRORL_TRY_INTERNAL(call)   \
+  do {                             \
+    int s_ = (call);               \
+    if (s_ != PRORL_OK) return s_; \
+  } while (0)
+
 #define PRORL_CUDA(call)                                      \
   do {                                                        \
     cudaError_t e_ = (call);                                  \
@@ -96,6 +102,9 @@ int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_strid
                 const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                 const prorl_loss_cfg* cfg, double n_global,
                 void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st);
+int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const void* weight, int64_t w_stride,
+                  int32_t d, int32_t vocab, const int32_t* targets, int64_t n_rows, float inv_temp, float* logp,
+                  float* entropy, cudaStream_t st);
 int launch_slab_reduce(const double* slab, int slab_rows, double* partials, cudaStream_t st);
 int launch_gen_logits(void* logits, int dtype, int64_t row_stride, int32_t vocab, int64_t n_rows,
                       int64_t row_key0, const int64_t* row_keys, const int32_t* targets, const float* old_lp, uint64_t seed,

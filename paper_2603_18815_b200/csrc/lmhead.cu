@@ -1,0 +1,325 @@
+// lmhead.cu — K6: fused LM head + logprob / entropy on the 5th-gen tensor
+// cores (SURVEY.md §8 f rank 2). The model forward is outside the reference's
+// scope; this kernel removes the logits round trip of K2: the
+// logits tile  X[128 rows x 256 vocab] = H[128 x d] . W[256 x d]^T  is
+// accumulated in TMEM by tcgen05.mma and consumed in place by an online
+// logsumexp epilogue, so the [rows x V] logits never reach HBM.
+//
+// CTA = one 128-row tile of hidden states, persistent over all V/256 vocab
+// tiles (the same order in every CTA, so the W tiles are shared through L2).
+// Warp roles (192 threads):
+//   warp 0      TMA producer (one elected lane): H / W tiles, 128B-swizzled
+//               (cp.async.bulk.tensor.2d, K-major, BK = 64 bf16 = one swizzle
+//               atom), STAGES-deep smem ring with full/empty mbarriers;
+//   warp 1      TMEM owner (tcgen05.alloc 512 columns = 2 accumulators of
+//               128 lanes x 256 fp32) and MMA issuer (one lane):
+//               tcgen05.mma.cta_group::1.kind::f16, M128 N256 K16, bf16 in,
+//               fp32 accumulate; tcgen05.commit frees smem stages and
+//               signals a finished accumulator;
+//   warps 2..5  epilogue: thread = one row (TMEM lane), tcgen05.ld 32 columns
+//               at a time, online base-2 logsumexp with the top element kept
+//               out of the sums (as K2), target-logit capture; the two TMEM
+//               accumulators let MMA of tile n+1 overlap the epilogue of n.
+// Output: logp / entropy per row, identical definitions to K2 (App. B.2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace prorl {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;  // 16 KB
+constexpr uint32_t B_BYTES = BN * BK * 2;  // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int kThreads = 192;
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr float kLog2e = 1.44269504088896340736f;
+
+struct LmParams {
+  int64_t n_rows;
+  int32_t vocab;
+  int32_t n_kb;      // d / BK
+  int32_t n_ntiles;  // ceil(V / BN)
+  float c;           // inv_temp * log2 e
+  const int32_t* targets;
+  float* logp;
+  float* entropy;
+};
+
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  // bounded spin: a protocol bug traps instead of hanging the GPU
+  for (uint64_t it = 0; !mbar_try_wait(bar, parity); ++it)
+    if (it > (1ull << 31)) __trap();
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem) {
+  const uint64_t addr = (smem_u32(smem) & 0x3FFFFu) >> 4;
+  return addr | (uint64_t(1) << 16)      // leading byte offset (unused for swizzled K-major) = 1
+         | (uint64_t(64) << 32)          // stride byte offset: 1024 B >> 4
+         | (uint64_t(1) << 46)           // descriptor version (sm_100)
+         | (uint64_t(2) << 61);          // layout: SWIZZLE_128B
+}
+
+// Instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4)          // D format f32
+                            | (1u << 7)        // A format bf16
+                            | (1u << 10)       // B format bf16
+                            | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_lmhead(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, const LmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the 128B-swizzle atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+  }
+  if (warp == 1) {  // whole warp: allocate 512 TMEM columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer =====
+      uint32_t s = 0, ph = 0;
+      for (int n = 0; n < p.n_ntiles; ++n) {
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          mbar_wait_bounded(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(sA + s * A_BYTES, &tmH, kb * BK, (int32_t)m0, &full[s]);
+          tma_load_2d(sB + s * B_BYTES, &tmW, kb * BK, n * BN, &full[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      uint32_t s = 0, ph = 0;
+      for (int n = 0; n < p.n_ntiles; ++n) {
+        const int acc = n & 1;
+        mbar_wait_bounded(&tempty[acc], ((n >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          mbar_wait_bounded(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ad = umma_desc_sw128(sA + s * A_BYTES);
+          const uint64_t bd = umma_desc_sw128(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // K = 16 per MMA: +32 B along the swizzle atom
+            umma_bf16(d_tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), (kb | k) != 0);
+          umma_commit(&empty[s]);  // smem stage free once these MMAs retire
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ===== epilogue: one row per thread =====
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    const int64_t grow = m0 + row;
+    const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
+    const float c = p.c;
+    float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, xy = 0.f;
+    for (int n = 0; n < p.n_ntiles; ++n) {
+      const int acc = n & 1;
+      mbar_wait_bounded(&tfull[acc], (n >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      const int col0 = n * BN;
+      const int ncols = min(BN, p.vocab - col0);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(base + (uint32_t)c0, v);
+        if (c0 >= ncols) continue;
+        const int lim = min(32, ncols - c0);
+        if (tgt >= col0 + c0 && tgt < col0 + c0 + lim) xy = v[tgt - col0 - c0];
+        float lm = v[0];
+#pragma unroll
+        for (int j = 1; j < 32; ++j) lm = j < lim ? fmaxf(lm, v[j]) : lm;
+        if (lm * c > Mc) {  // new top element: fold the old one in, rescale, exclude the new one
+          int pos = 0;
+#pragma unroll
+          for (int j = 31; j >= 0; --j) pos = (j < lim && v[j] == lm) ? j : pos;
+          const float nMc = lm * c;
+          if (Mc != -INFINITY) {
+            const float sc = ex2_approx(Mc - nMc), dl = nMc - Mc;
+            T = sc * fmaf(-dl, S, T);
+            S *= sc;
+            const float d = fmaf(Mx, c, -nMc), e = ex2_approx(d);
+            S += e;
+            T = fmaf(d, e, T);
+          }
+          Mc = nMc;
+          Mx = lm;
+          v[pos] = -INFINITY;  // excluded (handled analytically at the end)
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < lim && v[j] != -INFINITY) {
+            const float d = fmaf(v[j], c, -Mc), e = ex2_approx(d);
+            S += e;
+            T = fmaf(d, e, T);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);
+    }
+    if (grow < p.n_rows) {
+      const float r = fmaf(Mx, c, -Mc);
+      const float ir = ex2_approx(-r);
+      const float qq = S * ir;
+      const float l1q = log1pf(qq);
+      p.logp[grow] = (fmaf(xy, c, -Mc) - r) * kLn2 - l1q;
+      if (p.entropy) p.entropy[grow] = l1q + kLn2 * (fmaf(r, qq, -T * ir) / (1.f + qq));
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int32_t d, int64_t stride_elems, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(PRORL_E_CUDA, "lmhead: cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)stride_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PRORL_E_SHAPE, "lmhead: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return PRORL_OK;
+}
+
+}  // namespace
+
+int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const void* weight, int64_t w_stride,
+                  int32_t d, int32_t vocab, const int32_t* targets, int64_t n_rows, float inv_temp, float* logp,
+                  float* entropy, cudaStream_t st) {
+  (void)ctx;
+  if (d <= 0 || d % BK != 0) return fail(PRORL_E_SHAPE, "lmhead: hidden size must be a positive multiple of 64");
+  if (vocab <= 0 || n_rows < 0) return fail(PRORL_E_SHAPE, "lmhead: bad vocab / rows");
+  if (h_stride < d || w_stride < d || (h_stride * 2) % 16 || (w_stride * 2) % 16 ||
+      reinterpret_cast<uintptr_t>(hidden) % 16 || reinterpret_cast<uintptr_t>(weight) % 16)
+    return fail(PRORL_E_SHAPE, "lmhead: hidden/weight must be 16-B aligned with 16-B multiple row strides");
+  if (!(inv_temp > 0.f)) return fail(PRORL_E_MALFORMED_REQUEST, "lmhead: inv_temperature must be > 0");
+  if (n_rows == 0) return PRORL_OK;
+  CUtensorMap tmH, tmW;
+  PRORL_TRY_INTERNAL(make_map(&tmH, hidden, n_rows, d, h_stride, BM));
+  PRORL_TRY_INTERNAL(make_map(&tmW, weight, vocab, d, w_stride, BN));
+  LmParams p{};
+  p.n_rows = n_rows;
+  p.vocab = vocab;
+  p.n_kb = d / BK;
+  p.n_ntiles = (vocab + BN - 1) / BN;
+  p.c = inv_temp * kLog2e;
+  p.targets = targets;
+  p.logp = logp;
+  p.entropy = entropy;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+  PRORL_CUDA(cudaFuncSetAttribute(k_lmhead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)((n_rows + BM - 1) / BM);
+  k_lmhead<<<grid, kThreads, smem, st>>>(tmH, tmW, p);
+  PRORL_CUDA(cudaGetLastError());
+  return PRORL_OK;
+}
+
+}  // namespace prorl

@@ -167,6 +167,18 @@ class Scorer:
                                       _stream(stream)))
         return grad, dl
 
+    # ---- K6: fused LM head (tcgen05) ----
+    def lmhead_logprob(self, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor,
+                       inv_temp: float = 1.0, stream=None):
+        """logp / entropy of softmax(hidden @ weight.T * inv_temp) without materialising the logits."""
+        n, d = hidden.shape
+        V = weight.shape[0]
+        logp = torch.empty(n, dtype=torch.float32, device=hidden.device)
+        ent = torch.empty(n, dtype=torch.float32, device=hidden.device)
+        check(N.lib.prorl_lmhead_logprob(self.ctx, ptr(hidden), hidden.stride(0), ptr(weight), weight.stride(0), d, V,
+                                         ptr(targets), n, inv_temp, ptr(logp), ptr(ent), _stream(stream)))
+        return logp, ent
+
     # ---- synthetic LM head ----
     def gen_logits(self, out: torch.Tensor, n_rows: int, row_key0: int, targets=None, old_lp=None, seed: int = 0,
                    sigma: float = 2.0, vocab: int | None = None, stream=None) -> torch.Tensor:
