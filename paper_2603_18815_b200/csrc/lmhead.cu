@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t grow = m0 + row;
     const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
     const float c = p.c;
-    float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, xy = 0.f;
+    // Per row: ~V terms. Each 32-column group is summed in 4 chains, then added
+    // to the running (S, T) with Kahan compensation (cS, cT), so the fp32
+    // error stays at a few ulps over 150K+ terms.
+    float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, cS = 0.f, cT = 0.f, xy = 0.f;
     for (int n = 0; n < p.n_ntiles; ++n) {
       const int acc = n & 1;
       mbar_wait_bounded(&tfull[acc], (n >> 1) & 1);
@@ -212,35 +215,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(base + (uint32_t)c0, v);
         if (c0 >= ncols) continue;
         const int lim = min(32, ncols - c0);
-        if (tgt >= col0 + c0 && tgt < col0 + c0 + lim) xy = v[tgt - col0 - c0];
+        const int ty = tgt - col0 - c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xy = (j == ty) ? v[j] : xy;
         float lm = v[0];
 #pragma unroll
         for (int j = 1; j < 32; ++j) lm = j < lim ? fmaxf(lm, v[j]) : lm;
+        int excl = -1;
         if (lm * c > Mc) {  // new top element: fold the old one in, rescale, exclude the new one
-          int pos = 0;
 #pragma unroll
-          for (int j = 31; j >= 0; --j) pos = (j < lim && v[j] == lm) ? j : pos;
+          for (int j = 31; j >= 0; --j) excl = (j < lim && v[j] == lm) ? j : excl;
           const float nMc = lm * c;
           if (Mc != -INFINITY) {
             const float sc = ex2_approx(Mc - nMc), dl = nMc - Mc;
             T = sc * fmaf(-dl, S, T);
+            cT = sc * fmaf(-dl, cS, cT);
             S *= sc;
+            cS *= sc;
             const float d = fmaf(Mx, c, -nMc), e = ex2_approx(d);
-            S += e;
-            T = fmaf(d, e, T);
+            float y = e - cS, t = S + y;
+            cS = (t - S) - y;
+            S = t;
+            y = d * e - cT;
+            t = T + y;
+            cT = (t - T) - y;
+            T = t;
           }
           Mc = nMc;
           Mx = lm;
-          v[pos] = -INFINITY;  // excluded (handled analytically at the end)
         }
+        float gs[4] = {0.f, 0.f, 0.f, 0.f}, gt[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          if (j < lim && v[j] != -INFINITY) {
+          if (j < lim && j != excl) {
             const float d = fmaf(v[j], c, -Mc), e = ex2_approx(d);
-            S += e;
-            T = fmaf(d, e, T);
+            gs[j & 3] += e;
+            gt[j & 3] = fmaf(d, e, gt[j & 3]);
           }
         }
+        float y = ((gs[0] + gs[1]) + (gs[2] + gs[3])) - cS, t = S + y;
+        cS = (t - S) - y;
+        S = t;
+        y = ((gt[0] + gt[1]) + (gt[2] + gt[3])) - cT;
+        t = T + y;
+        cT = (t - T) - y;
+        T = t;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
