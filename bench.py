@@ -176,6 +176,35 @@ def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
             "frac_of_nominal_8000": gbs / 8000.0}
 
 
+def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
+    """K6 (fused LM head + logprob, SURVEY §8 f rank 2) at the Qwen3-4B LM-head
+    shape (d = 2560, V = config vocab): tcgen05 GEMM with the online-softmax
+    epilogue; logits never reach HBM. Reported beside the forward metric."""
+    import torch
+    n, d, V = 16384, 2560, c["vocab"]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    H = torch.randn(n, d, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, d, device="cuda", generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    t = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
+    sc.lmhead_logprob(H, W, t)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        sc.lmhead_logprob(H, W, t)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    tf = 2.0 * n * d * V / (ms / 1e3) / 1e12
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    burst = float(peaks.get("bf16_tflops", 1590.0))
+    sustained = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    del H, W
+    return {"kernel": "k_lmhead (K6: tcgen05 LM head + online logsumexp)", "rows": n, "d_model": d, "vocab": V,
+            "ms_per_launch": ms, "tflops": tf, "frac_of_measured_bf16_burst": tf / burst,
+            "frac_of_measured_bf16_sustained": tf / sustained, "rows_per_s": n / (ms / 1e3)}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path for this workload on the host
     cores (the oracle port — the reference has no implementation of the math,
@@ -272,6 +301,7 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and not args.no_backward else None
+    lmhead = measure_lmhead(sc, c, args) if not args.no_backward and c["dtype"] == "bf16" else None
     e2e_ms = ev0.elapsed_time(ev1)
     dev_ms = float(seg[1] + seg[2] + seg[3])  # pack+GRPO, score, all-reduce (inputs resident)
     score_ms = float(seg[2])
@@ -330,6 +360,7 @@ def run_ours(args):
                        "clip_hi_frac": res["clip_hi_frac"], "n_active": res["n_active"]},
             "cpu_baseline": cpu,
             "backward": backward,
+            "lmhead": lmhead,
         }
         print(json.dumps(line), flush=True)
     sc.close()
