@@ -260,7 +260,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = synth.CONFIGS[args.config]
-    shard = synth.make_shard(args.config, rank=rank, world=world)
+    # weak scaling: the global batch grows with the GPU count (tasks x N, same
+    # seed), groups are LPT-sharded so every rank scores ~one config-sized shard
+    gcfg = dict(c)
+    gcfg["tasks"] = c["tasks"] * world
+    shard = synth.make_shard(gcfg, rank=rank, world=world, seed=2603 + c["index"])
     host = shard.batch.pinned()
     cfg = ScoreConfig(vocab=c["vocab"], dtype=c["dtype"], microbatch_rows=args.microbatch)
     sc = Scorer(local)
@@ -354,6 +358,7 @@ def run_ours(args):
             "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": c["dtype"], "data": "synthetic",
             "config": {"workload": c["desc"], "config_id": args.config, "parallelism": f"group-sharded dp{world}",
+                       "tasks_global": gcfg["tasks"],
                        "global_batch": f"{len(shard.groups)} informative groups on rank0, {n_total} active rows",
                        "seq_len": c["tokens"], "vocab": c["vocab"], "microbatch_rows": args.microbatch,
                        "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
