@@ -516,8 +516,8 @@ struct K2Config {
 };
 constexpr K2Config kConfigs[] = {{"w16s2c4096g2", 16, 2, 4096, 2}, {"w16s2c4096g4", 16, 2, 4096, 4},
                                  {"w12s3c4096g2", 12, 3, 4096, 2}, {"w8s5c4096g2", 8, 5, 4096, 2},
-                                 {"w8s3c8192g4", 8, 3, 8192, 4}};
-constexpr int kDefaultConfig = 1;
+                                 {"w8s3c8192g4", 8, 3, 8192, 4}, {"w16s2c4096g8", 16, 2, 4096, 8}};
+constexpr int kDefaultConfig = 5;
 
 int active_config() {
   static int idx = [] {
@@ -553,7 +553,8 @@ int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* 
     case 1: return run_score_cfg<T, 16, 2, 4096, 4, FUSED>(a, grid, st);
     case 2: return run_score_cfg<T, 12, 3, 4096, 2, FUSED>(a, grid, st);
     case 3: return run_score_cfg<T, 8, 5, 4096, 2, FUSED>(a, grid, st);
-    default: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, st);
+    case 4: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, st);
+    default: return run_score_cfg<T, 16, 2, 4096, 8, FUSED>(a, grid, st);
   }
 }
 
