@@ -167,3 +167,46 @@ def test_oracle_against_live_reference_when_present():
         tol = float(rng.choice([0.0, 0.2]))
         args = (n, has.ctypes.data, failed.ctypes.data, w.ctypes.data, tol)
         assert L.oracle_is_informative(*args) == R.ref_is_informative(*args)
+
+
+# ---- oracle arithmetic vs an independent formulation (torch float64) -------------
+# The reference has no implementation of logprob / entropy ("parity
+# unpinned"); these pin the oracle's definitions to the
+# textbook formulation used by RL trainers (gathered log_softmax; entropy =
+# logsumexp - sum p x, as prime-rl's selective_log_softmax / compute_entropy).
+def test_oracle_logprob_entropy_vs_torch_float64():
+    import torch
+    rng = np.random.default_rng(0)
+    for V, it, scale in [(7, 1.0, 1.0), (1003, 1.0, 2.0), (32000, 1 / 0.7, 3.0), (4099, 2.0, 0.1)]:
+        n = 16
+        x = (rng.normal(0, scale, (n, V))).astype(np.float32)
+        x[3, ::5] = -np.inf                         # masked vocabulary entries
+        t = rng.integers(0, V, n).astype(np.int32)
+        t[3] = 1                                    # a finite target in the masked row
+        lp, ent = O.logprob_entropy(x, t, inv_temp=it)
+        xt = torch.from_numpy(x).double() * float(np.float32(it))  # the oracle takes inv_temp as float
+        ref_lp = torch.log_softmax(xt, 1).gather(1, torch.from_numpy(t).long()[:, None])[:, 0]
+        p = torch.softmax(xt, 1)
+        ref_ent = torch.logsumexp(xt, 1) - torch.nan_to_num(p * xt, nan=0.0).sum(1)
+        np.testing.assert_allclose(lp, ref_lp.numpy(), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(ent, ref_ent.numpy(), rtol=1e-10, atol=1e-10)
+
+
+def test_oracle_grpo_and_loss_hand_computed():
+    # group of 4 usable rewards [1, 0, 1, 0] (+ one FAILED): mean 0.5, std(ddof=1) = sqrt(1/3)
+    adv, info, asum, nr = O.grpo(np.array([1.0, 0.0, 1.0, 0.0, 1.0]), np.array([1, 1, 1, 1, 0], np.uint8),
+                                 np.array([0, 5], np.int32))
+    s = np.sqrt(1.0 / 3.0) + 1e-6
+    np.testing.assert_allclose(adv, [0.5 / s, -0.5 / s, 0.5 / s, -0.5 / s, 0.0], rtol=1e-12)
+    assert info.tolist() == [1] and nr == 4.0 and abs(asum) < 1e-12
+    # DAPO surrogate, ratio inside / below / above the clip range
+    logp = np.array([np.log(1.0), np.log(0.5), np.log(2.0), np.log(2.0)])
+    old = np.zeros(4, np.float32)
+    A = np.array([1.0, -1.0, 1.0, -1.0])
+    P, Q, nb = O.loss(logp, np.zeros(4), old, A, np.arange(4, dtype=np.int32), np.zeros(4, np.int16))
+    # l = -min(r A, clip(r, 0.8, 1.28) A): r=1 -> -1; r=0.5,A=-1 -> -min(-0.5,-0.8) = 0.8;
+    # r=2,A=1 -> -min(2, 1.28) = -1.28; r=2,A=-1 -> -min(-2,-1.28) = 2
+    lo, hi = 1.0 - float(np.float32(0.2)), 1.0 + float(np.float32(0.28))  # eps are float in the cfg
+    want = [-1.0, float(lo), -float(hi), 2.0]
+    np.testing.assert_allclose(P[0], sum(want), rtol=1e-12)
+    assert P[5] == 1 and P[6] == 1          # clip_lo (r<0.8, A<0), clip_hi (r>1.28, A>0)
