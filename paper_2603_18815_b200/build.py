@@ -60,21 +60,30 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + list(INCLUDE.glob("rollout/**/*.hpp"))
     objs = []
+    jobs = []
     for src in SOURCES:
         s = CSRC / src
         o = BUILD / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            if s.suffix == ".cpp":  # host-only C++: the host compiler directly, full optimisation
-                cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{INCLUDE}",
-                       f"-I{CSRC}", f"-I{json_include()}", "-I/usr/local/cuda/include", "-c", str(s), "-o", str(o)]
-            else:
-                cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{json_include()}", "-c", str(s), "-o", str(o)]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-            if verbose:
-                (BUILD / (s.stem + ".ptxas.txt")).write_text(r.stderr)
+            jobs.append((s, o))
+
+    def compile_one(job):
+        s, o = job
+        if s.suffix == ".cpp":  # host-only C++: the host compiler directly, full optimisation
+            cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{INCLUDE}",
+                   f"-I{CSRC}", f"-I{json_include()}", "-I/usr/local/cuda/include", "-c", str(s), "-o", str(o)]
+        else:
+            cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{json_include()}", "-c", str(s), "-o", str(o)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"compile failed for {s.name}:\n{r.stderr}")
+        if verbose:
+            (BUILD / (s.stem + ".ptxas.txt")).write_text(r.stderr)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, jobs))
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
