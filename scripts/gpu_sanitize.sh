@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_kernels.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -3 gpurun_out/sanitize_$tool.log
+done
