@@ -44,11 +44,27 @@ struct LmParams {
   int32_t vocab;
   int32_t n_kb;      // d / BK
   int32_t n_ntiles;  // ceil(V / BN)
+  int32_t m_tiles;   // ceil(n_rows / BM)
+  int32_t n_chunks;  // vocab chunks per row tile (work unit = row tile x vocab chunk)
+  int32_t tpc;       // vocab tiles per chunk
   float c;           // inv_temp * log2 e
   const int32_t* targets;
-  float* logp;
-  float* entropy;
+  float* part;       // [n_rows][n_chunks][6]: Mc, Mx, S, T, xy, has_y
 };
+
+// Work units u = chunk * m_tiles + m (chunk-major: CTAs running at the same
+// time mostly share one vocab chunk of W through L2); CTA b takes b, b+G, ...
+struct Unit {
+  int32_t m, chunk, t0, t1;  // row tile, vocab chunk, vocab tiles [t0, t1)
+};
+__device__ __forceinline__ Unit unit_of(const LmParams& p, int64_t u) {
+  Unit x;
+  x.chunk = (int32_t)(u / p.m_tiles);
+  x.m = (int32_t)(u - (int64_t)x.chunk * p.m_tiles);
+  x.t0 = x.chunk * p.tpc;
+  x.t1 = min(p.n_ntiles, x.t0 + p.tpc);
+  return x;
+}
 
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
   // bounded spin: a protocol bug traps instead of hanging the GPU
@@ -126,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n_units = (int64_t)p.m_tiles * p.n_chunks;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -154,15 +170,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
       uint32_t s = 0, ph = 0;
-      for (int n = 0; n < p.n_ntiles; ++n) {
-        for (int kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait_bounded(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          tma_load_2d(sA + s * A_BYTES, &tmH, kb * BK, (int32_t)m0, &full[s]);
-          tma_load_2d(sB + s * B_BYTES, &tmW, kb * BK, n * BN, &full[s]);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        for (int n = w.t0; n < w.t1; ++n) {
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait_bounded(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+            tma_load_2d(sA + s * A_BYTES, &tmH, kb * BK, w.m * BM, &full[s]);
+            tma_load_2d(sB + s * B_BYTES, &tmW, kb * BK, n * BN, &full[s]);
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
       }
@@ -170,9 +189,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ===== MMA issuer =====
       uint32_t s = 0, ph = 0;
-      for (int n = 0; n < p.n_ntiles; ++n) {
-        const int acc = n & 1;
-        mbar_wait_bounded(&tempty[acc], ((n >> 1) & 1) ^ 1);
+      int tile = 0;  // accumulator use counter across units
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+       const Unit w = unit_of(p, u);
+       for (int n = w.t0; n < w.t1; ++n, ++tile) {
+        const int acc = tile & 1;
+        mbar_wait_bounded(&tempty[acc], ((tile >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
         for (int kb = 0; kb < p.n_kb; ++kb) {
@@ -190,22 +212,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+       }
       }
     }
   } else {
     // ===== epilogue: one row per thread =====
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
-    const int64_t grow = m0 + row;
-    const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
     const float c = p.c;
+    int tile = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const Unit w = unit_of(p, u);
+    const int64_t grow = (int64_t)w.m * BM + row;
+    const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
+    bool has_y = false;
     // Per row: ~V terms. Each 32-column group is summed in 4 chains, then added
     // to the running (S, T) with Kahan compensation (cS, cT), so the fp32
     // error stays at a few ulps over 150K+ terms.
     float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, cS = 0.f, cT = 0.f, xy = 0.f;
-    for (int n = 0; n < p.n_ntiles; ++n) {
-      const int acc = n & 1;
-      mbar_wait_bounded(&tfull[acc], (n >> 1) & 1);
+    for (int n = w.t0; n < w.t1; ++n, ++tile) {
+      const int acc = tile & 1;
+      mbar_wait_bounded(&tfull[acc], (tile >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       const int col0 = n * BN;
@@ -216,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c0 >= ncols) continue;
         const int lim = min(32, ncols - c0);
         const int ty = tgt - col0 - c0;
+        if (ty >= 0 && ty < lim) has_y = true;
 #pragma unroll
         for (int j = 0; j < 32; ++j) xy = (j == ty) ? v[j] : xy;
         float lm = v[0];
@@ -264,14 +292,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
     }
-    if (grow < p.n_rows) {
-      const float r = fmaf(Mx, c, -Mc);
-      const float ir = ex2_approx(-r);
-      const float qq = S * ir;
-      const float l1q = log1pf(qq);
-      p.logp[grow] = (fmaf(xy, c, -Mc) - r) * kLn2 - l1q;
-      if (p.entropy) p.entropy[grow] = l1q + kLn2 * (fmaf(r, qq, -T * ir) / (1.f + qq));
+    if (grow < p.n_rows) {  // this unit's partial for (row, chunk)
+      float* o = p.part + ((size_t)grow * p.n_chunks + w.chunk) * 6;
+      o[0] = Mc;
+      o[1] = Mx;
+      o[2] = S;
+      o[3] = T;
+      o[4] = xy;
+      o[5] = has_y ? 1.f : 0.f;
     }
+    }  // units
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -280,6 +310,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+// Per row: merge the vocab-chunk partials (each chunk's top element is kept
+// out of its sums) into logp / entropy with the same exclusion trick as K2.
+__global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, int32_t n_chunks, float c,
+                               float* __restrict__ logp, float* __restrict__ entropy) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  const float* pr = part + (size_t)i * n_chunks * 6;
+  int g = 0;
+  float xy = 0.f;
+  for (int k = 0; k < n_chunks; ++k) {
+    if (pr[k * 6] > pr[g * 6]) g = k;
+    if (pr[k * 6 + 5] != 0.f) xy = pr[k * 6 + 4];
+  }
+  const float Mc = pr[g * 6], Mx = pr[g * 6 + 1];
+  float S = pr[g * 6 + 2], T = pr[g * 6 + 3];
+  for (int k = 0; k < n_chunks; ++k) {
+    if (k == g) continue;
+    const float mk = pr[k * 6];
+    if (mk == -INFINITY) continue;
+    const float rk = fmaf(pr[k * 6 + 1], c, -mk), ek = exp2f(rk);
+    const float Sk = pr[k * 6 + 2] + ek, Tk = fmaf(rk, ek, pr[k * 6 + 3]);  // fold the chunk's top in
+    const float sc = exp2f(mk - Mc), dl = Mc - mk;
+    S = fmaf(sc, Sk, S);
+    T = fmaf(sc, fmaf(-dl, Sk, Tk), T);
+  }
+  const float r = fmaf(Mx, c, -Mc);
+  const float ir = exp2f(-r);
+  const float q = S * ir;
+  const float l1q = log1pf(q);
+  logp[i] = (fmaf(xy, c, -Mc) - r) * kLn2 - l1q;
+  if (entropy) entropy[i] = l1q + kLn2 * (fmaf(r, q, -T * ir) / (1.f + q));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -313,7 +376,6 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int32_t d, int64_t 
 int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const void* weight, int64_t w_stride,
                   int32_t d, int32_t vocab, const int32_t* targets, int64_t n_rows, float inv_temp, float* logp,
                   float* entropy, cudaStream_t st) {
-  (void)ctx;
   if (d <= 0 || d % BK != 0) return fail(PRORL_E_SHAPE, "lmhead: hidden size must be a positive multiple of 64");
   if (vocab <= 0 || n_rows < 0) return fail(PRORL_E_SHAPE, "lmhead: bad vocab / rows");
   if (h_stride < d || w_stride < d || (h_stride * 2) % 16 || (w_stride * 2) % 16 ||
@@ -329,14 +391,40 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
   p.vocab = vocab;
   p.n_kb = d / BK;
   p.n_ntiles = (vocab + BN - 1) / BN;
+  p.m_tiles = (int32_t)((n_rows + BM - 1) / BM);
+  // Split the vocabulary into chunks so the (row tile x chunk) units balance
+  // over the SMs: pick the chunk count whose round-robin makespan
+  // ceil(units / n_sm) * tiles_per_chunk wastes the least SM time (chunks of
+  // >= 16 vocab tiles).
+  {
+    const int64_t total = (int64_t)p.m_tiles * p.n_ntiles;
+    double best = -1.0;
+    for (int32_t nch = 1; nch <= p.n_ntiles; ++nch) {
+      const int32_t tpc = (p.n_ntiles + nch - 1) / nch;
+      if (nch > 1 && tpc < 16) break;  // keep partial-merge traffic small (<= 1/16 of the tiles)
+      const int32_t chunks = (p.n_ntiles + tpc - 1) / tpc;
+      const int64_t units = (int64_t)p.m_tiles * chunks;
+      const int64_t g = std::min<int64_t>(units, ctx->n_sm);
+      const double eff = (double)total / ((double)g * (double)((units + g - 1) / g) * tpc) *
+                         ((double)g / ctx->n_sm);
+      if (eff > best + 1e-3) {
+        best = eff;
+        p.tpc = tpc;
+        p.n_chunks = chunks;
+      }
+    }
+  }
   p.c = inv_temp * kLog2e;
   p.targets = targets;
-  p.logp = logp;
-  p.entropy = entropy;
+  PRORL_CUDA(ctx->lm_part.ensure(sizeof(float) * 6 * (size_t)n_rows * (size_t)p.n_chunks));
+  p.part = ctx->lm_part.as<float>();
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
   PRORL_CUDA(cudaFuncSetAttribute(k_lmhead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const unsigned grid = (unsigned)((n_rows + BM - 1) / BM);
+  const int64_t units = (int64_t)p.m_tiles * p.n_chunks;
+  const unsigned grid = (unsigned)std::min<int64_t>(units, ctx->n_sm);
   k_lmhead<<<grid, kThreads, smem, st>>>(tmH, tmW, p);
+  PRORL_CUDA(cudaGetLastError());
+  k_lmhead_merge<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(p.part, n_rows, p.n_chunks, p.c, logp, entropy);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
 }
