@@ -395,6 +395,7 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   if (G) PRORL_CUDA(cudaMemcpyAsync(c->h_goff.p, hb->group_off, sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, st));
   PRORL_CUDA(cudaMemsetAsync(partials, 0, sizeof(double) * PRORL_N_PARTIALS, st));
   PRORL_CUDA(cudaMemsetAsync(slab, 0, sizeof(double) * PRORL_N_PARTIALS * srows, st));
+  PRORL_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int) * ERR_N, st));  // no stale flags from an aborted call
   PRORL_CUDA(cudaEventRecord(c->ev[1], st));
 
   // ---- K1 pack, K3 grpo ----
@@ -427,7 +428,9 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
     if (pool->provide) {
       const int rc = pool->provide(pool->user, row0, n, pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
                                    pk.act_target + row0, pk.act_old_lp + row0, &buf, &stride, stream);
-      if (rc != PRORL_OK) return rc;
+      if (rc != PRORL_OK)
+        return fail(rc, "prorl_score_host: logits callback failed with status " + std::to_string(rc) +
+                            " at micro-batch " + std::to_string(j));
       if (!buf) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: logits callback returned null");
     } else {
       void* b = pool->buffers[j % pool->n_pool];

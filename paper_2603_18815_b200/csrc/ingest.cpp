@@ -150,16 +150,17 @@ class Scanner {
       return;
     }
   }
-  void skip() {
+  void skip(int depth = 0) {
     ws();
     if (p_ >= e_) fail("unexpected end");
+    if (depth > 64) fail("nesting too deep");
     const char c = *p_;
     if (c == '"') {
       str();
     } else if (c == '{') {
-      object([&](std::string_view) { skip(); });
+      object([&](std::string_view) { skip(depth + 1); });
     } else if (c == '[') {
-      array([&] { skip(); });
+      array([&] { skip(depth + 1); });
     } else if (c == 't' || c == 'f' || c == 'n') {
       const char* lit = c == 't' ? "true" : (c == 'f' ? "false" : "null");
       const size_t n = std::strlen(lit);
