@@ -417,3 +417,61 @@ def test_full_c2_properties_and_sampled_rows(scorer, cuda):
         lps.append(lp.item()); ents.append(ent.item()); olps.append(olp[0]); oents.append(oent[0])
     assert_rows_close(lps, olps, "sampled logp")
     assert_rows_close(ents, oents, "sampled entropy")
+
+
+# ---------------------------------------------------------------- randomized ragged batches
+def _random_batch(rng, V):
+    n_seq = int(rng.integers(1, 40))
+    turns, ids, lps = [], [], []
+    src = 0
+    for s in range(n_seq):
+        if rng.random() < 0.15:
+            continue                      # FAILED / dropped slot: empty sequence
+        for _ in range(int(rng.integers(1, 12))):
+            role = int(rng.choice([0, 1, 2, 2, 3]))
+            L = int(rng.choice([0, 1, 2, int(rng.integers(1, 300))]))
+            turns.append((src, s, L, role))
+            ids.append(rng.integers(0, V, L))
+            lps.append(-rng.random(L) * 4 if role == 2 else np.zeros(L))
+            src += L
+    t = np.zeros(len(turns), N.TURN_DTYPE)
+    if turns:
+        arr = np.array(turns, np.int64)
+        t["src_off"], t["traj"], t["len"], t["role"] = arr[:, 0], arr[:, 1], arr[:, 2], arr[:, 3]
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+    return t, cat(ids, np.int64), cat(lps, np.float64), n_seq
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_pack_random_ragged_batches(scorer, cuda, seed):
+    rng = np.random.default_rng(1000 + seed)
+    V = int(rng.choice([50, 32000, 151936]))
+    t, ids, lp, n_seq = _random_batch(rng, V)
+    st, ora = O.pack(t, ids, lp, n_seq, V)
+    assert st == 0
+    compare_pack(scorer.pack(t, dev(ids, cuda), dev(lp, cuda), n_seq, V, ora["n_active"]), ora)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_score_host_random_ragged_batches(scorer, cuda, seed):
+    rng = np.random.default_rng(2000 + seed)
+    V = int(rng.choice([97, 1003, 4096]))
+    t, ids, lp, n_seq = _random_batch(rng, V)
+    # groups of random sizes over the slots, random binary rewards, a few FAILED
+    sizes, left = [], n_seq
+    while left > 0:
+        k = int(min(left, rng.integers(1, 6)))
+        sizes.append(k)
+        left -= k
+    goff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    reward = rng.choice([0.0, 1.0], n_seq)
+    usable = (rng.random(n_seq) > 0.1).astype(np.uint8)
+    b = HostBatchArrays(t, ids, lp, reward, usable, goff)
+    cfg = ScoreConfig(vocab=V, dtype="bf16", microbatch_rows=257)
+    pool = [torch.empty((257, V), dtype=torch.bfloat16, device=cuda)]
+    got, _ = scorer.score_host(b, cfg, pool, fill=True, seed=seed)
+    st, ora = O.pack(t, ids, lp, n_seq, V)
+    hb = O.host_batch(t, ids, lp, reward, usable, goff)
+    ref = O.score_batch(hb, O.score_cfg(V, "bf16", microbatch_rows=257), seed, 2.0, nthreads=4)
+    assert ref["status"] == 0 and ref["n_active"] == ora["n_active"]
+    assert_partials_close(got, ref["partials"], ref["abs"], ref["n_border"], f"ragged{seed}")
