@@ -5,6 +5,7 @@
 // drops the trajectory today, proj/src/trainer/harness.cpp:263-273).
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -82,6 +83,12 @@ static int nccl_fail(ncclResult_t r, const char* what) {
   } while (0)
 
 static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// NVTX range for profilers (nsys / ncu --nvtx); header-only, no-op without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Host-side count of active rows: a policy token at position > 0 of its
 // sequence makes the previous row active.
@@ -378,6 +385,7 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
 
   double* partials = c->partials.as<double>();
   double* slab = c->slab.as<double>();
+  NvtxRange step_range("prorl_score_host");
   PRORL_CUDA(cudaEventRecord(c->ev[0], st));
   // ---- H2D ----
   if (hb->n_turns)
