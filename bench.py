@@ -195,6 +195,19 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    # the unfused baseline it replaces: cuBLAS bf16 GEMM writing the logits to HBM, then K2
+    logits = torch.empty((n, V), dtype=torch.bfloat16, device="cuda")
+    torch.matmul(H, W.T, out=logits)
+    sc.logprob_entropy(logits, t)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(H, W.T, out=logits)
+        sc.logprob_entropy(logits, t)
+    e1.record()
+    torch.cuda.synchronize()
+    unfused_ms = e0.elapsed_time(e1) / reps
+    del logits
     tf = 2.0 * n * d * V / (ms / 1e3) / 1e12
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     burst = float(peaks.get("bf16_tflops", 1590.0))
@@ -202,7 +215,9 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
     del H, W
     return {"kernel": "k_lmhead (K6: tcgen05 LM head + online logsumexp)", "rows": n, "d_model": d, "vocab": V,
             "ms_per_launch": ms, "tflops": tf, "frac_of_measured_bf16_burst": tf / burst,
-            "frac_of_measured_bf16_sustained": tf / sustained, "rows_per_s": n / (ms / 1e3)}
+            "frac_of_measured_bf16_sustained": tf / sustained, "rows_per_s": n / (ms / 1e3),
+            "unfused_cublas_gemm_plus_k2_ms": unfused_ms, "speedup_vs_unfused": unfused_ms / ms,
+            "logits_bytes_avoided": n * V * 2}
 
 
 def run_reference(args):
@@ -292,9 +307,13 @@ def run_ours(args):
 
     # totals over ranks (weak scaling: each rank scores its own groups)
     n_local = torch.tensor([shard.n_active], dtype=torch.float64, device="cuda")
+    per_rank = [shard.n_active]
     if world > 1:
-        dist.all_reduce(n_local)
-    n_total = int(n_local.item())
+        gathered = [torch.zeros_like(n_local) for _ in range(world)]
+        dist.all_gather(gathered, n_local)
+        per_rank = [int(x.item()) for x in gathered]
+    n_total = int(sum(per_rank))
+    lpt_imbalance = max(per_rank) / (sum(per_rank) / len(per_rank))
 
     clocks = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -358,7 +377,7 @@ def run_ours(args):
             "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": c["dtype"], "data": "synthetic",
             "config": {"workload": c["desc"], "config_id": args.config, "parallelism": f"group-sharded dp{world}",
-                       "tasks_global": gcfg["tasks"],
+                       "tasks_global": gcfg["tasks"], "lpt_imbalance_max_over_mean": lpt_imbalance,
                        "global_batch": f"{len(shard.groups)} informative groups on rank0, {n_total} active rows",
                        "seq_len": c["tokens"], "vocab": c["vocab"], "microbatch_rows": args.microbatch,
                        "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
