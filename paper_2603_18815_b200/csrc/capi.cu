@@ -347,9 +347,21 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
   if (hb->n_groups > 0 && hb->group_off[hb->n_groups] != hb->n_rollouts)
     return fail(PRORL_E_SHAPE, "prorl_score_host: group_off[n_groups] != n_rollouts");
+  // host-side validation of the descriptors (the device buffers are sized from
+  // them, so inconsistent input must be rejected before any kernel runs)
   int64_t tok = 0;
-  for (int64_t t = 0; t < hb->n_turns; ++t) tok += hb->turns[t].len;
+  for (int64_t t = 0; t < hb->n_turns; ++t) {
+    const prorl_turn_desc& d = hb->turns[t];
+    if (d.traj < 0 || d.traj >= hb->n_rollouts || d.len < 0 || d.role > PRORL_ROLE_TOOL ||
+        (t > 0 && d.traj < hb->turns[t - 1].traj) || d.src_off < 0 || d.src_off + d.len > hb->n_tokens)
+      return fail(PRORL_E_SHAPE, "prorl_score_host: turn " + std::to_string(t) +
+                                     " out of order / out of range (traj, len, role or src_off)");
+    tok += d.len;
+  }
   if (tok != hb->n_tokens) return fail(PRORL_E_SHAPE, "prorl_score_host: n_tokens != sum of turn lengths");
+  for (int32_t g = 0; g < hb->n_groups; ++g)
+    if (hb->group_off[g] < 0 || hb->group_off[g] > hb->group_off[g + 1])
+      return fail(PRORL_E_SHAPE, "prorl_score_host: group_off not monotone in [0, n_rollouts]");
   PRORL_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = S(stream);
   const int64_t N = hb->n_tokens, A = host_active_rows(hb->turns, hb->n_turns);

@@ -475,3 +475,24 @@ def test_score_host_random_ragged_batches(scorer, cuda, seed):
     ref = O.score_batch(hb, O.score_cfg(V, "bf16", microbatch_rows=257), seed, 2.0, nthreads=4)
     assert ref["status"] == 0 and ref["n_active"] == ora["n_active"]
     assert_partials_close(got, ref["partials"], ref["abs"], ref["n_border"], f"ragged{seed}")
+
+
+def test_score_host_rejects_inconsistent_descriptors(scorer, cuda):
+    sh = synth.make_shard("c1")
+    b = sh.batch
+    cfg = _cfg("c1")
+    pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.float32, device=cuda)]
+    t = b.turns.copy()
+    t["traj"][0], t["traj"][-1] = t["traj"][-1], t["traj"][0]        # unsorted
+    with pytest.raises(RolloutError) as e:
+        scorer.score_host(HostBatchArrays(t, b.ids, b.lp, b.reward, b.usable, b.group_off), cfg, pool, fill=True)
+    assert e.value.code == "shape_mismatch"
+    t = b.turns.copy()
+    t["src_off"][3] = len(b.ids)                                      # points past the ids
+    with pytest.raises(RolloutError):
+        scorer.score_host(HostBatchArrays(t, b.ids, b.lp, b.reward, b.usable, b.group_off), cfg, pool, fill=True)
+    g = b.group_off.copy()
+    g[1] = g[2] + 1                                                    # not monotone
+    with pytest.raises(RolloutError):
+        scorer.score_host(HostBatchArrays(b.turns, b.ids, b.lp, b.reward, b.usable, g), cfg, pool, fill=True)
+    scorer.score_host(b, cfg, pool, fill=True)                         # ctx still usable
