@@ -478,7 +478,8 @@ def test_score_host_random_ragged_batches(scorer, cuda, seed):
 
 
 def test_score_host_rejects_inconsistent_descriptors(scorer, cuda):
-    sh = synth.make_shard("c1")
+    sh = synth.make_shard("c1", seed=99)
+    assert len(sh.batch.group_off) >= 3
     b = sh.batch
     cfg = _cfg("c1")
     pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.float32, device=cuda)]
