@@ -16,6 +16,9 @@
 // buffer may alias the logits (in-place backward): every chunk is in shared
 // memory before its region is overwritten, and the target logit is read at
 // row start.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "stream.cuh"
 
@@ -159,17 +162,40 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
   }
 }
 
-constexpr int kGradWarps = 16, kGradStages = 2, kGradChunk = 4096;
+// Launch configurations (warps/CTA x stages x chunk bytes), PRORL_K5_CONFIG selects.
+template <typename T, int W, int ST, int CH>
+int run_grad_cfg(const GradArgs& a, int n_sm, cudaStream_t st) {
+  auto kern = k_grad<T, W, ST, CH>;
+  constexpr size_t smem = (size_t)W * ST * CH + (size_t)W * ST * 8;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::min<int64_t>((int64_t)n_sm, (a.n_rows + W - 1) / W);
+  kern<<<grid, W * 32, smem, st>>>(a);
+  PRORL_CUDA(cudaGetLastError());
+  return PRORL_OK;
+}
+
+int grad_config() {
+  static int idx = [] {
+    const char* e = std::getenv("PRORL_K5_CONFIG");
+    if (!e) return 2;  // default: 12 warps x 4 stages (best of the sweep, scripts/k5_sweep.py)
+    const char* names[] = {"w16s2c4096", "w16s3c4096", "w12s4c4096", "w8s6c4096", "w16s4c2048"};
+    for (int i = 0; i < 5; ++i)
+      if (std::strcmp(e, names[i]) == 0) return i;
+    return 2;
+  }();
+  return idx;
+}
 
 template <typename T>
 int run_grad(const GradArgs& a, int n_sm, cudaStream_t st) {
-  auto kern = k_grad<T, kGradWarps, kGradStages, kGradChunk>;
-  constexpr size_t smem = (size_t)kGradWarps * kGradStages * kGradChunk + (size_t)kGradWarps * kGradStages * 8;
-  PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = (int)std::min<int64_t>((int64_t)n_sm, (a.n_rows + kGradWarps - 1) / kGradWarps);
-  kern<<<grid, kGradWarps * 32, smem, st>>>(a);
-  PRORL_CUDA(cudaGetLastError());
-  return PRORL_OK;
+  switch (grad_config()) {
+    case 1: return run_grad_cfg<T, 16, 3, 4096>(a, n_sm, st);
+    case 2: return run_grad_cfg<T, 12, 4, 4096>(a, n_sm, st);
+    case 3: return run_grad_cfg<T, 8, 6, 4096>(a, n_sm, st);
+    case 4: return run_grad_cfg<T, 16, 4, 2048>(a, n_sm, st);
+    default: return run_grad_cfg<T, 16, 2, 4096>(a, n_sm, st);
+  }
 }
 
 }  // namespace
