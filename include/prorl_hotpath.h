@@ -291,10 +291,19 @@ typedef int (*prorl_logits_fn)(void* user, int64_t row0, int64_t n, const int32_
                                const int32_t* d_seq, const int32_t* d_cu_seqlens,
                                const int32_t* d_targets, const float* d_old_lp,
                                const void** d_logits, int64_t* row_stride, void* stream);
+/* If `provide_hidden` is set instead, the step runs the fused LM head (K6):
+ * the callback returns the micro-batch's final hidden states (bf16
+ * [n x d_model], row stride *h_stride) and the library computes logp /
+ * entropy against `weight` (bf16 [vocab x d_model], row stride w_stride) on
+ * the tensor cores, then the loss (K4); the logits are never materialised. */
+typedef int (*prorl_hidden_fn)(void* user, int64_t row0, int64_t n, const int32_t* d_rows,
+                               const int32_t* d_seq, const int32_t* d_cu_seqlens,
+                               const void** d_hidden, int64_t* h_stride, void* stream);
 typedef struct prorl_logits_pool {
   void* const* buffers; int32_t n_pool; int32_t fill; int64_t row_stride;
   uint64_t seed; float sigma; int32_t pad_;
   prorl_logits_fn provide; void* user;
+  prorl_hidden_fn provide_hidden; const void* weight; int64_t w_stride; int32_t d_model; int32_t pad2_;
 } prorl_logits_pool;
 
 /* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for

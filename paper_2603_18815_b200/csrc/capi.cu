@@ -111,6 +111,15 @@ static int64_t host_active_rows(const prorl_turn_desc* turns, int64_t n_turns) {
 
 using namespace prorl;
 
+// ABI layout guards (mirrored by tests/test_abi.py against the ctypes structs)
+static_assert(sizeof(prorl_turn_desc) == 24, "prorl_turn_desc layout");
+static_assert(sizeof(prorl_packed) == 13 * 8, "prorl_packed layout");
+static_assert(sizeof(prorl_loss_cfg) == 16, "prorl_loss_cfg layout");
+static_assert(sizeof(prorl_score_cfg) == 40, "prorl_score_cfg layout");
+static_assert(sizeof(prorl_host_batch) == 88, "prorl_host_batch layout");
+static_assert(sizeof(prorl_logits_pool) == 88, "prorl_logits_pool layout");
+static_assert(sizeof(prorl_ingest_result) == 112, "prorl_ingest_result layout");
+
 extern "C" {
 
 int prorl_abi_version(void) { return PRORL_ABI_VERSION; }
@@ -340,8 +349,11 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
                      const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream) {
   if (!c || !hb || !cfg || !pool || !host_partials)
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null argument");
-  if (!pool->provide && (pool->n_pool < 1 || !pool->buffers))
+  const bool lmhead_mode = pool->provide_hidden != nullptr;
+  if (!lmhead_mode && !pool->provide && (pool->n_pool < 1 || !pool->buffers))
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: empty logits pool");
+  if (lmhead_mode && (!pool->weight || pool->d_model <= 0))
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: lm-head mode needs weight and d_model");
   if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
@@ -394,6 +406,11 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   PRORL_CUDA(c->informative.ensure((size_t)std::max(G, 1)));
   PRORL_CUDA(c->partials.ensure(sizeof(double) * PRORL_N_PARTIALS));
   PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(srows, loss_slab_rows(c))));
+  if (lmhead_mode) {
+    const size_t mbr = (size_t)std::max<int64_t>(std::min<int64_t>(A, cfg->microbatch_rows), 1);
+    PRORL_CUDA(c->logp.ensure(sizeof(float) * mbr));
+    PRORL_CUDA(c->entropy.ensure(sizeof(float) * mbr));
+  }
 
   double* partials = c->partials.as<double>();
   double* slab = c->slab.as<double>();
@@ -439,10 +456,29 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
                         cfg->adv_eps, 0.0, c->adv.as<float>(), c->informative.as<uint8_t>(), partials, st));
   PRORL_CUDA(cudaEventRecord(c->ev[2], st));
 
-  // ---- K2+K4 over logits micro-batches ----
+  // ---- K2+K4 over logits micro-batches (or K6 + K4 from hidden states) ----
   const int64_t mb = cfg->microbatch_rows;
   for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
     const int64_t n = std::min(mb, A - row0);
+    if (lmhead_mode) {
+      const void* hid = nullptr;
+      int64_t hs = pool->d_model;
+      const int rc = pool->provide_hidden(pool->user, row0, n, pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
+                                          &hid, &hs, stream);
+      if (rc != PRORL_OK)
+        return fail(rc, "prorl_score_host: hidden-state callback failed with status " + std::to_string(rc) +
+                            " at micro-batch " + std::to_string(j));
+      if (!hid) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: hidden-state callback returned null");
+      float* lp = c->logp.as<float>();
+      float* en = c->entropy.as<float>();
+      PRORL_TRY(launch_lmhead(c, hid, hs, pool->weight, pool->w_stride, pool->d_model, cfg->vocab,
+                              pk.act_target + row0, n, cfg->inv_temperature, lp, en, st));
+      int used = 0;
+      PRORL_TRY(launch_loss(c, lp, en, pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0,
+                            pk.act_turn + row0, nullptr, n, &cfg->loss, slab, loss_slab_rows(c), &used, st));
+      PRORL_TRY(launch_slab_reduce(slab, used, partials, st));
+      continue;
+    }
     const void* buf = nullptr;
     int64_t stride = pool->row_stride;
     if (pool->provide) {
@@ -467,7 +503,7 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
                            pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
   }
-  PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
+  if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
   PRORL_CUDA(cudaEventRecord(c->ev[3], st));
   PRORL_TRY(prorl_allreduce(c, partials, PRORL_N_PARTIALS, stream));
   PRORL_CUDA(cudaEventRecord(c->ev[4], st));

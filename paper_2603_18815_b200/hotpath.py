@@ -209,13 +209,40 @@ class Scorer:
     def allreduce(self, partials: torch.Tensor, stream=None) -> None:
         check(N.lib.prorl_allreduce(self.ctx, ptr(partials), partials.numel(), _stream(stream)))
 
+    def score_host_lmhead(self, batch: "HostBatchArrays", cfg: ScoreConfig, hidden_fn, weight: torch.Tensor,
+                          stream=None):
+        """Whole step with the fused LM head (K6): hidden_fn(row0, n, rows, seq, cu) -> bf16 [n x d] device
+        tensor (kept alive until the next call); weight bf16 [V x d]."""
+        keep = []
+
+        def cb(user, row0, n, rows, seq, cu, out_ptr, out_stride, strm):
+            try:
+                h = hidden_fn(row0, n, rows, seq, cu)
+                keep[:] = [h]
+                out_ptr[0] = h.data_ptr()
+                out_stride[0] = h.stride(0)
+                return 0
+            except Exception:  # noqa: BLE001 — reported as a C status
+                return -3
+        fn = N.HIDDEN_FN(cb)
+        hb = batch.c()
+        dummy = (C.c_void_p * 1)(None)
+        lp = N.LogitsPool(C.cast(dummy, C.c_void_p), 0, 0, 0, 0, 0.0, 0, None, None,
+                          C.cast(fn, C.c_void_p), ptr(weight), weight.stride(0), weight.shape[1], 0)
+        out = np.zeros(N.N_PARTIALS, dtype=np.float64)
+        tm = np.zeros(5, dtype=np.float32)
+        sc = cfg.c()
+        check(N.lib.prorl_score_host(self.ctx, C.byref(hb), C.byref(sc), C.byref(lp), ptr(out), ptr(tm),
+                                     _stream(stream)))
+        return out, tm
+
     # ---- whole per-GPU step from host buffers ----
     def score_host(self, batch: "HostBatchArrays", cfg: ScoreConfig, pool: list[torch.Tensor], fill: bool,
                    seed: int = 0, sigma: float = 2.0, stream=None):
         hb = batch.c()
         bufs = (C.c_void_p * len(pool))(*[ptr(b) for b in pool])
         lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0,
-                          None, None)
+                          None, None, None, None, 0, 0, 0)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()

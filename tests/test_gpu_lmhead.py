@@ -70,3 +70,33 @@ def test_lmhead_throughput_report(scorer, cuda):
     tflops = 2.0 * n * d * V / (ms / 1e3) / 1e12
     print(f"\nK6 lmhead: {n} rows x d {d} x V {V}: {ms:.2f} ms, {tflops:.0f} TFLOP/s, {n / ms * 1e3 / 1e6:.2f} M rows/s")
     assert tflops > 50
+
+
+def test_score_host_lmhead_mode_matches_materialised_logits(scorer, cuda):
+    """Whole step with the fused LM head (hidden-state source) == the same step
+    on the explicitly materialised logits (pool source, K2+K4)."""
+    from paper_2603_18815_b200 import _native as N
+    from paper_2603_18815_b200 import synth
+    from paper_2603_18815_b200.hotpath import ScoreConfig
+    sh = synth.make_shard("c1", seed=99)
+    b = sh.batch
+    V, d, A = 32000, 256, sh.n_active
+    g = torch.Generator(device=cuda).manual_seed(3)
+    H = torch.randn(A, d, generator=g, device=cuda).to(torch.bfloat16)
+    W = (torch.randn(V, d, generator=g, device=cuda) * (3.0 / d ** 0.5)).to(torch.bfloat16)
+    calls = []
+
+    def hidden_fn(row0, n, rows, seq, cu):
+        calls.append((row0, n))
+        return H[row0:row0 + n]
+
+    got, _ = scorer.score_host_lmhead(b, ScoreConfig(vocab=V, dtype="bf16", microbatch_rows=1000), hidden_fn, W)
+    assert calls[0] == (0, 1000) and sum(n for _, n in calls) == A
+    logits = (H.double() @ W.double().T).float().contiguous()
+    ref, _ = scorer.score_host(b, ScoreConfig(vocab=V, dtype="fp32", microbatch_rows=A), [logits], fill=False)
+    assert got[N.P_N_ACTIVE] == ref[N.P_N_ACTIVE] == A
+    for i in range(N.N_PARTIALS):
+        if i in (N.P_CLIP_LO, N.P_CLIP_HI) or (i >= N.N_GLOBAL and (i - N.N_GLOBAL) % 5 == 4):
+            assert abs(got[i] - ref[i]) <= 2, (i, got[i], ref[i])
+        else:
+            assert abs(got[i] - ref[i]) <= 1e-5 * max(abs(ref[i]), 1.0), (i, got[i], ref[i])
