@@ -220,6 +220,30 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
             "logits_bytes_avoided": n * V * 2}
 
 
+def measure_lmhead_step(sc, host, cfg, c, reps: int = 2) -> dict:
+    """The whole step (pack, GRPO, K6 fused LM head + K4 loss, all-reduce) on the
+    same shard with a hidden-state source instead of logits (d = 2560): the
+    logits of the 0.9 M active rows never exist in HBM."""
+    import torch
+    from paper_2603_18815_b200.hotpath import ScoreConfig
+    d, V = 2560, c["vocab"]
+    H = torch.randn(cfg.microbatch_rows, d, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(V, d, device="cuda") * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    lcfg = ScoreConfig(vocab=V, dtype="bf16", microbatch_rows=cfg.microbatch_rows)
+    fn = lambda row0, n, rows, seq, cu: H[:n]  # noqa: E731 — stand-in for the model's final hidden states
+    sc.score_host_lmhead(host, lcfg, fn, W)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    seg = np.zeros(5)
+    for _ in range(reps):
+        _, tm = sc.score_host_lmhead(host, lcfg, fn, W)
+        seg += tm
+    wall = (time.perf_counter() - t0) / reps
+    del H, W
+    return {"path": "prorl_score_host with a hidden-state source (K1, K3, K6 tcgen05 LM head + K4, all-reduce)",
+            "d_model": d, "ms_per_step_device": float(seg[1] + seg[2] + seg[3]) / reps, "ms_per_step_wall": wall * 1e3}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path for this workload on the host
     cores (the oracle port — the reference has no implementation of the math,
@@ -337,6 +361,12 @@ def run_ours(args):
     clk = clocks.stop()
     backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and not args.no_backward else None
     lmhead = measure_lmhead(sc, c, args) if not args.no_backward and c["dtype"] == "bf16" else None
+    lmhead_step = None
+    if lmhead is not None:
+        del pool  # free the 15 GB logits pool: this path never materialises logits
+        torch.cuda.empty_cache()
+        lmhead_step = measure_lmhead_step(sc, host, cfg, c)
+        lmhead_step["masked_tokens_per_s"] = shard.n_active / (lmhead_step["ms_per_step_device"] / 1e3)
     e2e_ms = ev0.elapsed_time(ev1)
     dev_ms = float(seg[1] + seg[2] + seg[3])  # pack+GRPO, score, all-reduce (inputs resident)
     score_ms = float(seg[2])
@@ -397,6 +427,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "backward": backward,
             "lmhead": lmhead,
+            "lmhead_step": lmhead_step,
         }
         print(json.dumps(line), flush=True)
     sc.close()
