@@ -139,6 +139,9 @@ class DeviceScorer {
                            void* stream = nullptr);
   ScoreResult score_batch(const HostBatch& batch, LogitsSource& logits, const ScoreConfig& cfg,
                           void* stream = nullptr);
+  // Same on a raw C-ABI batch view (e.g. from ingest_responses).
+  ScoreResult score_view(const prorl_host_batch& batch, LogitsSource& logits, const ScoreConfig& cfg,
+                         void* stream = nullptr);
 
   prorl_ctx* ctx() const { return ctx_; }
 
@@ -152,6 +155,23 @@ class DeviceScorer {
 TokenTrajectory trajectory_from_json(const nlohmann::json& turns);
 // The fields the reference harness records (harness.cpp:254-273) plus the trajectory.
 RolloutOutcome outcome_from_response(const nlohmann::json& response);
+
+// Wire JSON of one shard's /process responses -> host SoA (prorl_ingest_responses):
+// group g owns responses [group_off[g], group_off[g+1]).
+class IngestedBatch {
+ public:
+  IngestedBatch(const std::vector<std::string>& responses, const std::vector<std::int32_t>& group_off,
+                double gate_tolerance = 0.0, int threads = 0);
+  ~IngestedBatch();
+  IngestedBatch(const IngestedBatch&) = delete;
+  IngestedBatch& operator=(const IngestedBatch&) = delete;
+  const prorl_host_batch& view() const { return r_.batch; }
+  std::int64_t n_active() const { return r_.n_active; }
+  int n_informative() const { return r_.n_informative; }
+
+ private:
+  prorl_ingest_result r_{};
+};
 
 // Throws the rollout::Error subclass for a C-ABI status (no-op for PRORL_OK).
 void throw_status(int status);

@@ -188,6 +188,27 @@ int provide_logits(void* user, std::int64_t row0, std::int64_t n, const std::int
 
 ScoreResult DeviceScorer::score_batch(const HostBatch& batch, LogitsSource& logits, const ScoreConfig& cfg,
                                       void* stream) {
+  return score_view(batch.view(), logits, cfg, stream);
+}
+
+IngestedBatch::IngestedBatch(const std::vector<std::string>& responses, const std::vector<std::int32_t>& group_off,
+                             double gate_tolerance, int threads) {
+  std::vector<const char*> ptrs(responses.size());
+  std::vector<size_t> lens(responses.size());
+  for (size_t i = 0; i < responses.size(); ++i) {
+    ptrs[i] = responses[i].data();
+    lens[i] = responses[i].size();
+  }
+  if (group_off.empty() || (size_t)group_off.back() != responses.size())
+    throw MalformedRequest("IngestedBatch: group_off must end at the number of responses");
+  throw_status(prorl_ingest_responses(ptrs.data(), lens.data(), group_off.data(), (std::int32_t)group_off.size() - 1,
+                                      gate_tolerance, threads, &r_));
+}
+
+IngestedBatch::~IngestedBatch() { prorl_ingest_free(&r_); }
+
+ScoreResult DeviceScorer::score_view(const prorl_host_batch& hb, LogitsSource& logits, const ScoreConfig& cfg,
+                                     void* stream) {
   prorl_score_cfg c{};
   c.loss.eps_lo = cfg.eps_lo;
   c.loss.eps_hi = cfg.eps_hi;
@@ -203,7 +224,6 @@ ScoreResult DeviceScorer::score_batch(const HostBatch& batch, LogitsSource& logi
   prorl_logits_pool pool{};
   pool.provide = &provide_logits;
   pool.user = &tr;
-  const prorl_host_batch hb = batch.view();
   double partials[PRORL_N_PARTIALS];
   float tm[5];
   const int st = prorl_score_host(ctx_, &hb, &c, &pool, partials, tm, stream);

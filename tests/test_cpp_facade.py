@@ -57,3 +57,32 @@ def test_cpp_score_groups_vs_oracle(binary):
     assert got[N.P_N_ACTIVE] == P[N.P_N_ACTIVE]
     assert got[N.P_N_ROLLOUTS] == P[N.P_N_ROLLOUTS]
     assert abs(got[N.P_CLIP_LO] - P[N.P_CLIP_LO]) <= ref["n_border"]
+
+
+@pytest.mark.gpu
+def test_cpp_score_responses_tool_vs_oracle(tmp_path):
+    """tools/score_responses: wire JSON -> IngestedBatch -> DeviceScorer, all in C++."""
+    from paper_2603_18815_b200 import synth
+    from tests.wire import to_responses
+    B.build()
+    exe = ROOT / "build" / "score_responses"
+    src = ROOT / "tools" / "score_responses.cpp"
+    if not exe.exists() or exe.stat().st_mtime < max(src.stat().st_mtime, B.LIB.stat().st_mtime):
+        subprocess.run(["g++", "-std=c++17", "-O2", f"-I{ROOT / 'include'}", f"-I{B.json_include()}", str(src),
+                        "-o", str(exe), f"-L{B.PKG}", "-lprorl_hotpath", f"-Wl,-rpath,{B.PKG}"], check=True)
+    sh = synth.make_shard("c1", seed=99)
+    b = sh.batch
+    assert all(b.group_off[1:] - b.group_off[:-1] == 4)
+    path = tmp_path / "responses.jsonl"
+    path.write_bytes(b"\n".join(to_responses(b)) + b"\n")
+    r = subprocess.run([str(exe), str(path), "4", "32000", "fp32", "21"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["n_active"] == sh.n_active
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off)  # keys = slot index, as the tool
+    ref = O.score_batch(hb, O.score_cfg(32000, "fp32", microbatch_rows=4096), 21, 2.0, nthreads=4)
+    got = np.array(d["partials"])
+    P, Q = ref["partials"], ref["abs"]
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM, N.P_KL1_SUM):
+        assert abs(got[i] - P[i]) <= 1e-5 * Q[i], (i, got[i], P[i])
+    assert got[N.P_N_ACTIVE] == P[N.P_N_ACTIVE] and got[N.P_N_ROLLOUTS] == P[N.P_N_ROLLOUTS]

@@ -54,8 +54,7 @@ def _check(b, exp):
 
 @pytest.mark.parametrize("group_size", [1, 2, 3, 4, 24])
 def test_reference_wire_json(group_size):
-    cases = [c for c in GOLD["process_response"]
-             if all(not (r == 2) or True for r in c["roles"])]
+    cases = GOLD["process_response"]
     group_off = list(range(0, len(cases) + 1, group_size))
     if group_off[-1] != len(cases):
         group_off.append(len(cases))
@@ -67,24 +66,10 @@ def test_reference_wire_json(group_size):
 
 def test_synthetic_shard_roundtrip():
     """A synthetic shard serialised in the reference's schema ingests back to the same SoA."""
+    from tests.wire import to_responses
     sh = synth.make_shard("c1", seed=99)
     b = sh.batch
-    resp = []
-    starts = {}
-    for k, t in enumerate(b.turns):
-        starts.setdefault(int(t["traj"]), []).append(k)
-    for s in range(b.n_rollouts):
-        traj = []
-        for k in starts.get(s, []):
-            t = b.turns[k]
-            o, L, r = int(t["src_off"]), int(t["len"]), int(t["role"])
-            ids = b.ids[o:o + L].tolist()
-            traj.append({"input_ids": [] if r == 2 else ids, "logprobs": b.lp[o:o + L].tolist() if r == 2 else [],
-                         "output_ids": ids if r == 2 else [], "role": ["system", "user", "assistant", "tool"][r],
-                         "text": "tool said \"hi\" \\ é"})
-        resp.append(json.dumps({"job_id": f"j{s}", "status": "DONE" if b.usable[s] else "FAILED",
-                                "reward": float(b.reward[s]), "trajectory": traj,
-                                "timings": {"init_seconds": 0.0}}).encode())
+    resp = to_responses(b)
     got, n_active, n_info = ingest_responses(resp, b.group_off)
     for f in ("ids", "lp", "reward", "usable"):
         assert np.array_equal(getattr(got, f), getattr(b, f)), f
