@@ -220,6 +220,27 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
             "logits_bytes_avoided": n * V * 2}
 
 
+def measure_ingest(shard, reps: int = 3) -> dict:
+    """Wire side of the step: the shard's /process responses (reference schema,
+    handlers.cpp:57-91, serialised here) -> host SoA by the native parser on all
+    host threads (prorl_ingest_responses). Host-only; reported beside the device
+    step it would feed (it overlaps the previous step in a pipelined trainer)."""
+    from paper_2603_18815_b200.hotpath import ingest_responses
+    from tests.wire import to_responses
+    b = shard.batch
+    resp = to_responses(b)
+    nbytes = sum(len(r) for r in resp)
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        got, n_active, _ = ingest_responses(resp, b.group_off)
+        best = min(best, time.perf_counter() - t0)
+    assert n_active == shard.n_active and len(got.ids) == len(b.ids)
+    return {"wire_bytes": nbytes, "tokens": int(len(b.ids)), "ms": best * 1e3, "threads": os.cpu_count(),
+            "wire_gb_per_s": nbytes / best / 1e9, "tokens_per_s": len(b.ids) / best,
+            "masked_tokens_per_s": shard.n_active / best}
+
+
 def measure_lmhead_step(sc, host, cfg, c, reps: int = 2) -> dict:
     """The whole step (pack, GRPO, K6 fused LM head + K4 loss, all-reduce) on the
     same shard with a hidden-state source instead of logits (d = 2560): the
@@ -395,6 +416,12 @@ def run_ours(args):
     if rank == 0:
         res = finalize(partials)
         cpu = None
+        ingest = None
+        if world == 1 and not args.no_backward:
+            try:
+                ingest = measure_ingest(shard)
+            except Exception as ex:
+                ingest = {"error": repr(ex)}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 cpu = cpu_baseline(shard, cfg, 2603, args.cpu_seconds)
@@ -428,6 +455,7 @@ def run_ours(args):
             "backward": backward,
             "lmhead": lmhead,
             "lmhead_step": lmhead_step,
+            "ingest": ingest,
         }
         print(json.dumps(line), flush=True)
     sc.close()

@@ -292,7 +292,7 @@ int prorl_nccl_init(prorl_ctx* c, int nranks, int rank, const uint8_t* id128) {
 
 int prorl_allreduce(prorl_ctx* c, double* partials_dev, int n, void* stream) {
   if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_allreduce: null ctx");
-  if (!c->nccl_comm || c->nranks == 1 || n <= 0) return PRORL_OK;
+  if (!c->nccl_comm || n <= 0) return PRORL_OK;  // a 1-rank communicator still runs (tests the NCCL plumbing)
   PRORL_CUDA(cudaSetDevice(c->device));
   PRORL_NCCL(nccl().all_reduce(partials_dev, partials_dev, (size_t)n, ncclDouble, ncclSum,
                            static_cast<ncclComm_t>(c->nccl_comm), S(stream)));

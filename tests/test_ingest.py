@@ -128,3 +128,69 @@ def test_throughput_c2_sized():
     print(f"ingest: {nbytes / 1e6:.1f} MB, {len(b.ids) / 1e6:.2f} M tokens in {dt * 1e3:.1f} ms "
           f"({nbytes / dt / 1e9:.2f} GB/s)")
     assert nbytes / dt > 50e6
+
+
+def _turn_json(role, ids, lps_text=None):
+    if role == "assistant":
+        return (f'{{"input_ids":[],"logprobs":[{",".join(lps_text)}],"output_ids":[{",".join(map(str, ids))}],'
+                f'"role":"assistant"}}')
+    return f'{{"input_ids":[{", ".join(map(str, ids))}],"logprobs":[],"output_ids":[],"role":"{role}"}}'
+
+
+def test_logprob_decimal_parsing_is_exact():
+    """Every decimal shape a serialiser produces (shortest repr of doubles and of
+    float32 values, %.17g, exponents, 19+ digits, -0.0) parses to the double
+    Python's float() gives — bit-exact, including the x87 fast path's fallbacks."""
+    rng = np.random.default_rng(7)
+    vals = np.concatenate([
+        -rng.exponential(2.0, 4000),
+        -rng.exponential(2.0, 4000).astype(np.float32).astype(np.float64),
+        -(10.0 ** rng.uniform(-12, 2, 4000)),
+        np.round(-rng.exponential(2.0, 2000), 4),
+    ])
+    texts = []
+    for k, v in enumerate(vals):
+        m = k % 5
+        texts.append(repr(float(v)) if m < 2 else ("%.17g" % v if m == 2 else
+                     ("%.19f" % v if m == 3 else "%.21e" % v)))
+    texts += ["-0.0", "0", "-1", "-1e-300", "-2.2250738585072014e-308", "-123456789012345678901234.5",
+              "-0.00000000000000000000000000123", "-1.0000000000000002", "-0.99999999999999999999"]
+    want = [float(t) for t in texts]
+    ids = list(range(1, len(texts) + 1))
+    resp = (f'{{"status":"DONE","reward":1,"trajectory":[{_turn_json("user", [5])},'
+            f'{_turn_json("assistant", ids, texts)}]}}').encode()
+    other = b'{"status":"DONE","reward":0,"trajectory":[{"role":"user","input_ids":[1]}]}'
+    b, _, _ = ingest_responses([resp, other], [0, 2])
+    got = b.lp[1:1 + len(texts)]
+    assert np.array_equal(got.view(np.uint64), np.array(want).view(np.uint64))
+
+
+def test_failed_members_are_compacted_out():
+    """FAILED rollouts inside an informative group are dropped from the token
+    stream (harness.cpp:84-90) while the group keeps their reward slots."""
+    def resp(status, reward, ids):
+        return (f'{{"status":"{status}","reward":{reward},"trajectory":[{_turn_json("user", ids[:2])},'
+                f'{_turn_json("assistant", ids[2:], [repr(-0.5 - 0.1 * i) for i in range(len(ids) - 2)])}]}}').encode()
+    rs = [resp("FAILED", 1.0, [9, 9, 9, 9]), resp("DONE", 1.0, [1, 2, 3, 4, 5]), resp("FAILED", 0.0, [8, 8, 8]),
+          resp("DONE", 0.0, [6, 7, 8]), resp("FAILED", 0.5, [7, 7, 7, 7, 7])]
+    b, n_active, n_info = ingest_responses(rs, [0, 5], threads=1)
+    assert n_info == 1
+    assert b.ids.tolist() == [1, 2, 3, 4, 5, 6, 7, 8]
+    assert [(int(t["src_off"]), int(t["traj"]), int(t["len"])) for t in b.turns] == [(0, 1, 2), (2, 1, 3), (5, 3, 2), (7, 3, 1)]
+    assert b.usable.tolist() == [0, 1, 0, 1, 0]
+    assert n_active == 3 + 1
+    assert b.lp.tolist() == [0.0, 0.0, -0.5, -0.6, -0.7, 0.0, 0.0, -0.5]
+
+
+@pytest.mark.parametrize("n_threads", [1, 2, 3, 8])
+def test_thread_split_is_invariant(n_threads):
+    from tests.wire import to_responses
+    sh = synth.make_shard("c1", seed=11)
+    b = sh.batch
+    resp = to_responses(b)
+    got, n_active, n_info = ingest_responses(resp, b.group_off, threads=n_threads)
+    ref, n_active1, n_info1 = ingest_responses(resp, b.group_off, threads=1)
+    assert (n_active, n_info) == (n_active1, n_info1)
+    for f in ("ids", "lp", "reward", "usable"):
+        assert np.array_equal(getattr(got, f), getattr(ref, f)), f
+    assert np.array_equal(got.turns, ref.turns)
