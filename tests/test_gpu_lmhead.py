@@ -38,6 +38,58 @@ def test_lmhead_vs_torch_fp64(scorer, cuda, n, d, V, inv_temp):
     _check(ent, rent, "entropy")
 
 
+@pytest.mark.parametrize("n,d,V,scale,pad", [
+    (1, 64, 1, 1.0, 0),        # one row, one vocabulary entry (logp = 0, H = 0)
+    (5, 64, 7, 1.0, 0),        # V far below one 256-wide vocabulary chunk
+    (130, 128, 257, 1.0, 0),   # one row and one vocab entry past a tile edge
+    (257, 192, 5000, 40.0, 0),  # peaked softmax: logits spread over hundreds of nats
+    (96, 320, 3001, 1.0, 64),  # hidden rows strided (padded leading dimension)
+])
+def test_lmhead_edges(scorer, cuda, n, d, V, scale, pad):
+    g = torch.Generator(device=cuda).manual_seed(7 * n + V)
+    Hfull = torch.randn(n, d + pad, device=cuda, generator=g).to(torch.bfloat16)
+    H = Hfull[:, :d]
+    W = (torch.randn(V, d, device=cuda, generator=g) * (scale / d ** 0.5)).to(torch.bfloat16)
+    t = torch.randint(0, V, (n,), device=cuda, dtype=torch.int32, generator=g)
+    if scale > 1:  # half the targets at the row's arg-max: logp -> 0 must keep its relative accuracy
+        x = H.double() @ W.double().T
+        t[::2] = x.argmax(dim=1).to(torch.int32)[::2]
+    lp, ent = scorer.lmhead_logprob(H, W, t)
+    rlp, rent = _ref(H, W, t, 1.0)
+    if V == 1:
+        assert torch.all(lp == 0) and torch.all(ent.abs() <= 1e-6)
+        return
+    if scale == 1.0:
+        _check(lp, rlp, "logp")
+        _check(ent, rent, "entropy")
+        return
+    # Peaked rows: the fp32 tensor-core accumulation of each logit (d products,
+    # |x| up to ~150) perturbs x_v by up to ~u32 * sum_i |h_i w_vi|, and
+    # logp = x_y - lse moves by at most twice that (SURVEY.md App. B.2 is exact
+    # only for given logits; K6 computes them). Tolerance = the 1e-5 relative
+    # bar plus that GEMM rounding bound.
+    gemm = 2.0 * 2.0 ** -24 * (H.double().abs() @ W.double().abs().T).max(dim=1).values
+    tol = 1e-5 * torch.clamp(rlp.abs(), min=1e-3) + gemm
+    err = (lp.double() - rlp).abs()
+    assert torch.all(err <= tol), ("logp", float((err / tol).max()))
+    etol = 1e-5 * torch.clamp(rent, min=1e-3) + gemm * (1.0 + rent)
+    assert torch.all((ent.double() - rent).abs() <= etol), "entropy"
+
+
+def test_lmhead_empty_and_shape_errors(scorer, cuda):
+    from paper_2603_18815_b200.hotpath import RolloutError
+    W = torch.zeros(100, 64, device=cuda, dtype=torch.bfloat16)
+    H = torch.zeros(0, 64, device=cuda, dtype=torch.bfloat16)
+    t = torch.zeros(0, device=cuda, dtype=torch.int32)
+    lp, ent = scorer.lmhead_logprob(H, W, t)
+    assert lp.numel() == 0
+    with pytest.raises(RolloutError) as e:
+        scorer.lmhead_logprob(torch.zeros(4, 96, device=cuda, dtype=torch.bfloat16),
+                              torch.zeros(100, 96, device=cuda, dtype=torch.bfloat16),
+                              torch.zeros(4, device=cuda, dtype=torch.int32))
+    assert e.value.code == "shape_mismatch"
+
+
 def test_lmhead_matches_k2_on_materialised_logits(scorer, cuda):
     """Same rows through K6 and through K2 on explicitly materialised fp32 logits."""
     n, d, V = 256, 1024, 32000
