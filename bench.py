@@ -19,7 +19,7 @@ j reads buffer j % 3, so no L2 reuse between micro-batches. Generation is not
 inside the timed region.
 
 Multi-GPU (torchrun): groups are sharded by deterministic LPT (no data-path
-collective); the only collective is the NCCL all-reduce of the 330-double
+collective); the only collective is the NCCL all-reduce of the 332-double
 partials inside each step. Timing is the max over ranks.
 """
 from __future__ import annotations

@@ -16,7 +16,7 @@
  * The arithmetic the reference does not have follows the
  * definitions fixed in SURVEY.md Appendix B and is computed in fp64:
  *   - logprob / entropy (B.2), GRPO advantage (B.3), DAPO clipped surrogate
- *     (B.4), metrics and the 330-double partials layout (B.5, B.6).
+ *     (B.4), metrics and the 332-double partials layout (B.5, B.6).
  * Parity status: packing / gate / generators are PINNED against the compiled
  * reference (oracle/_ref, tests/test_oracle_ref.py) and the reference's own
  * golden vectors (tests/golden/); logprob / entropy / advantage / loss are a

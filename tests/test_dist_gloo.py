@@ -2,7 +2,7 @@
 sharding, disjoint/complete shards, and the partials all-reduce.
 
 Each rank scores its own groups with the CPU oracle (the device path is
-replaced by the oracle here: there is no GPU) and the 330-double partials are
+replaced by the oracle here: there is no GPU) and the 332-double partials are
 summed with torch.distributed (gloo), exactly as prorl_allreduce sums them over
 NCCL on the GPUs. Because GRPO statistics are per group and the synthetic
 logits of a row are keyed by (global rollout, position), the all-reduced
