@@ -427,7 +427,7 @@ def run_ours(args):
                 cpu = cpu_baseline(shard, cfg, 2603, args.cpu_seconds)
             except Exception as ex:  # the baseline must not sink the GPU number
                 cpu = {"error": repr(ex)}
-        launches_per_step = 6 + 3 + 1 + n_mb + 1  # 2 scans x3, seq_bounds/pack/compact, grpo, score x n_mb, reduce
+        launches_per_step = 6 + 3 + 1 + n_mb + 1 + 1  # 2 scans x3, seq_bounds/pack/compact, grpo, score x n_mb, reduce, fold-errors
         line = {
             "metric": "masked tokens/sec scored (logprob+GRPO loss)",
             "value": value, "unit": "masked tokens/s", "n_gpus": world, "steps": K, "warmup": args.warmup,

@@ -24,7 +24,7 @@
  *   - every function returns 0 (PRORL_OK) or a negative prorl_status; the
  *     message is in prorl_last_error() (thread-local);
  *   - negative codes map 1:1 onto rollout::Error codes (errors.hpp:10-59) plus
- *     three new ones (cuda_error, nccl_error, shape_mismatch);
+ *     four new ones (cuda_error, nccl_error, shape_mismatch, peer_failed);
  *   - buffers are caller-owned device memory unless a name says host_; the
  *     library only owns the workspace inside a ctx;
  *   - all device work is stream-ordered on the stream argument, no implicit
@@ -53,6 +53,7 @@ typedef enum prorl_status {
   PRORL_E_NCCL = -11,             /* new: "nccl_error"      */
   PRORL_E_SHAPE = -12,            /* new: "shape_mismatch"  */
   PRORL_E_TOKEN_RANGE = -13,      /* new: "shape_mismatch" (token id outside [0,V)) */
+  PRORL_E_PEER_FAILED = -14,      /* new: "peer_failed" — another rank's step failed (see prorl_score_host) */
 } prorl_status;
 
 typedef enum prorl_dtype { PRORL_BF16 = 0, PRORL_FP32 = 1 } prorl_dtype;
@@ -68,8 +69,8 @@ enum { PRORL_ROLE_SYSTEM = 0, PRORL_ROLE_USER = 1, PRORL_ROLE_ASSISTANT = 2, PRO
 enum {
   PRORL_P_LOSS_SUM = 0, PRORL_P_N_ACTIVE = 1, PRORL_P_ENTROPY_SUM = 2, PRORL_P_LOGP_SUM = 3,
   PRORL_P_RATIO_SUM = 4, PRORL_P_CLIP_LO = 5, PRORL_P_CLIP_HI = 6, PRORL_P_KL1_SUM = 7,
-  PRORL_P_ADV_SUM = 8, PRORL_P_N_ROLLOUTS = 9, PRORL_P_KL_SUM = 10 /* sum of k3 KL vs the reference policy */
-  /* 11: reserved (0) */
+  PRORL_P_ADV_SUM = 8, PRORL_P_N_ROLLOUTS = 9, PRORL_P_KL_SUM = 10, /* sum of k3 KL vs the reference policy */
+  PRORL_P_ERR_RANKS = 11 /* ranks whose step failed (0 on success); summed by the all-reduce */
 };
 /* per-turn bucket k starts at PRORL_N_GLOBAL + 5*k: [N_k, loss_k, H_k, logp_k, clip_k] */
 
@@ -310,7 +311,12 @@ typedef struct prorl_logits_pool {
  * each micro-batch K2+K4 (fused), NCCL all-reduce (if initialised), D2H of
  * the partials into host_partials[PRORL_N_PARTIALS]. Synchronises `stream`.
  * timings_ms (nullable, [5]): h2d, pack+grpo, score (K2+K4 launches + slab
- * reduce, incl. generation when pool->fill), allreduce, d2h. */
+ * reduce, incl. generation when pool->fill), allreduce, d2h.
+ * Collective-safe failure: with a communicator of > 1 ranks every rank takes
+ * part in exactly one all-reduce per call, even when its own step fails
+ * (host validation, a callback, a device-side check): it contributes zeros
+ * with partials[PRORL_P_ERR_RANKS] = 1. No rank hangs; the failing rank
+ * returns its own status, the others PRORL_E_PEER_FAILED. */
 int prorl_score_host(prorl_ctx* ctx, const prorl_host_batch* batch, const prorl_score_cfg* cfg,
                      const prorl_logits_pool* logits, double* host_partials, float* timings_ms,
                      void* stream);

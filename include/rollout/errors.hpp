@@ -2,7 +2,7 @@
 // (proj/include/rollout/errors.hpp:10-59): every domain error derives from
 // rollout::Error and carries a stable machine-readable code(). This header
 // declares the codes the trainer-side scoring path raises or forwards, plus
-// the three it adds (cuda_error, nccl_error, shape_mismatch).
+// the four it adds (cuda_error, nccl_error, shape_mismatch, peer_failed).
 #pragma once
 
 #include <stdexcept>
@@ -31,6 +31,7 @@ inline constexpr char kIncompleteGroup[] = "incomplete_group";
 inline constexpr char kCudaError[] = "cuda_error";
 inline constexpr char kNcclError[] = "nccl_error";
 inline constexpr char kShapeMismatch[] = "shape_mismatch";
+inline constexpr char kPeerFailed[] = "peer_failed";
 }  // namespace detail
 
 // Reference codes used on this path (errors.hpp:208, 232, 237 in the reference).
@@ -41,5 +42,7 @@ struct IncompleteGroup : detail::CodedError<detail::kIncompleteGroup> { using Co
 struct CudaError : detail::CodedError<detail::kCudaError> { using CodedError::CodedError; };
 struct NcclError : detail::CodedError<detail::kNcclError> { using CodedError::CodedError; };
 struct ShapeMismatch : detail::CodedError<detail::kShapeMismatch> { using CodedError::CodedError; };
+// Another rank's step failed; this rank's all-reduced result is void.
+struct PeerFailed : detail::CodedError<detail::kPeerFailed> { using CodedError::CodedError; };
 
 }  // namespace rollout

@@ -20,7 +20,7 @@ ROLE_SYSTEM, ROLE_USER, ROLE_ASSISTANT, ROLE_TOOL = 0, 1, 2, 3
 TURN_BUCKETS, N_GLOBAL, N_PER_TURN = 64, 12, 5
 N_PARTIALS = N_GLOBAL + TURN_BUCKETS * N_PER_TURN
 (P_LOSS_SUM, P_N_ACTIVE, P_ENTROPY_SUM, P_LOGP_SUM, P_RATIO_SUM, P_CLIP_LO, P_CLIP_HI,
- P_KL1_SUM, P_ADV_SUM, P_N_ROLLOUTS, P_KL_SUM) = range(11)
+ P_KL1_SUM, P_ADV_SUM, P_N_ROLLOUTS, P_KL_SUM, P_ERR_RANKS) = range(12)
 
 # Turn descriptor: must match prorl_turn_desc (24 bytes).
 TURN_DTYPE = np.dtype([("src_off", "<i8"), ("traj", "<i4"), ("len", "<i4"), ("role", "u1"), ("pad", "u1", (7,))])

@@ -138,6 +138,7 @@ const char* prorl_status_code(int status) {
     case PRORL_E_NCCL: return "nccl_error";
     case PRORL_E_SHAPE: return "shape_mismatch";
     case PRORL_E_TOKEN_RANGE: return "shape_mismatch";
+    case PRORL_E_PEER_FAILED: return "peer_failed";
   }
   return "unknown";
 }
@@ -345,9 +346,48 @@ int prorl_shard_lpt(int32_t n_groups, const int64_t* load, int32_t world, int32_
   return PRORL_OK;
 }
 
+namespace {
+// Folds the device-side validation flags of this step into the partials before
+// the all-reduce, so a rank whose kernels rejected their input fails every rank.
+__global__ void k_fold_errors(const int* __restrict__ err, double* __restrict__ partials) {
+  int any = 0;
+#pragma unroll
+  for (int k = 0; k < prorl::ERR_N; ++k) any |= err[k];
+  if (any) partials[PRORL_P_ERR_RANKS] += 1.0;
+}
+
+int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_cfg* cfg,
+                    const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream,
+                    bool& reduced);
+}  // namespace
+
 int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_cfg* cfg,
                      const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream) {
-  if (!c || !hb || !cfg || !pool || !host_partials)
+  if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null ctx");
+  bool reduced = false;
+  const int rc = score_host_impl(c, hb, cfg, pool, host_partials, timings_ms, stream, reduced);
+  if (rc == PRORL_OK || reduced || !c->nccl_comm || c->nranks < 2) return rc;
+  // This rank failed before its all-reduce: still take part in it, with zeros
+  // and the failure flag, so the peers return PRORL_E_PEER_FAILED instead of
+  // waiting forever. The original status and message are kept.
+  const std::string msg = prorl_last_error();
+  cudaStream_t st = S(stream);
+  if (cudaSetDevice(c->device) == cudaSuccess && c->partials.ensure(sizeof(double) * PRORL_N_PARTIALS) == cudaSuccess) {
+    double* d = c->partials.as<double>();
+    static const double kOne = 1.0;
+    if (cudaMemsetAsync(d, 0, sizeof(double) * PRORL_N_PARTIALS, st) == cudaSuccess &&
+        cudaMemcpyAsync(d + PRORL_P_ERR_RANKS, &kOne, sizeof(double), cudaMemcpyHostToDevice, st) == cudaSuccess)
+      nccl().all_reduce(d, d, (size_t)PRORL_N_PARTIALS, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->nccl_comm), st);
+    cudaStreamSynchronize(st);
+  }
+  return fail(rc, msg);
+}
+
+namespace {
+int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_cfg* cfg,
+                    const prorl_logits_pool* pool, double* host_partials, float* timings_ms, void* stream,
+                    bool& reduced) {
+  if (!hb || !cfg || !pool || !host_partials)
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null argument");
   const bool lmhead_mode = pool->provide_hidden != nullptr;
   if (!lmhead_mode && !pool->provide && (pool->n_pool < 1 || !pool->buffers))
@@ -357,6 +397,9 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
+  if ((hb->n_turns > 0 && !hb->turns) || (hb->n_tokens > 0 && (!hb->ids || !hb->lp)) ||
+      (hb->n_rollouts > 0 && (!hb->reward || !hb->usable)) || (hb->n_groups > 0 && !hb->group_off))
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: null host array with a non-zero size");
   if (hb->n_groups > 0 && hb->group_off[hb->n_groups] != hb->n_rollouts)
     return fail(PRORL_E_SHAPE, "prorl_score_host: group_off[n_groups] != n_rollouts");
   // host-side validation of the descriptors (the device buffers are sized from
@@ -504,16 +547,23 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
   }
   if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
+  k_fold_errors<<<1, 1, 0, st>>>(c->d_err, partials);
+  PRORL_CUDA(cudaGetLastError());
   PRORL_CUDA(cudaEventRecord(c->ev[3], st));
+  reduced = true;  // from here on every rank has entered (or failed inside) the collective
   PRORL_TRY(prorl_allreduce(c, partials, PRORL_N_PARTIALS, stream));
   PRORL_CUDA(cudaEventRecord(c->ev[4], st));
   PRORL_CUDA(cudaMemcpyAsync(host_partials, partials, sizeof(double) * PRORL_N_PARTIALS, cudaMemcpyDeviceToHost, st));
   PRORL_CUDA(cudaEventRecord(c->ev[5], st));
   PRORL_TRY(prorl_check_errors(c, stream));
+  if (host_partials[PRORL_P_ERR_RANKS] > 0.0)
+    return fail(PRORL_E_PEER_FAILED, "peer_failed: " + std::to_string((int)host_partials[PRORL_P_ERR_RANKS]) +
+                                         " rank(s) failed this step; the all-reduced partials are void");
   if (timings_ms) {
     for (int k = 0; k < 5; ++k) PRORL_CUDA(cudaEventElapsedTime(&timings_ms[k], c->ev[k], c->ev[k + 1]));
   }
   return PRORL_OK;
 }
+}  // namespace
 
 }  // extern "C"

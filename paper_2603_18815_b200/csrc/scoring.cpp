@@ -18,6 +18,7 @@ void throw_status(int status) {
     case PRORL_E_MALFORMED_REQUEST: throw MalformedRequest(msg);
     case PRORL_E_CUDA: throw CudaError(msg);
     case PRORL_E_NCCL: throw NcclError(msg);
+    case PRORL_E_PEER_FAILED: throw PeerFailed(msg);
     default: throw ShapeMismatch(msg);
   }
 }

@@ -33,6 +33,7 @@ def test_abi_version_and_codes():
     assert N.lib.prorl_status_code(-10) == b"cuda_error"
     assert N.lib.prorl_status_code(-11) == b"nccl_error"
     assert N.lib.prorl_status_code(-12) == b"shape_mismatch"
+    assert N.lib.prorl_status_code(-14) == b"peer_failed"
 
 
 def test_struct_layouts_match_header():

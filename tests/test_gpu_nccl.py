@@ -45,3 +45,30 @@ def test_nccl_init_rejects_bad_rank(cuda):
         sc.nccl_init(1, 3, nccl_unique_id())
     # the context stays usable
     sc.nccl_init(1, 0, nccl_unique_id())
+
+
+def test_failed_step_sets_error_rank_flag(cuda):
+    """A device-side rejection (token id >= vocab) is folded into
+    partials[PRORL_P_ERR_RANKS] before the all-reduce, so with >1 ranks every
+    peer would fail with peer_failed instead of summing a void shard; a host
+    validation failure still enters the collective (no hang) and keeps its own
+    status. At world size 1 the flag comes back to this rank."""
+    from paper_2603_18815_b200.hotpath import HostBatchArrays
+    sh = synth.make_shard("c1", seed=5)
+    b = sh.batch
+    cfg = ScoreConfig(vocab=32000, dtype="fp32", microbatch_rows=2048)
+    pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.float32, device=cuda)]
+    sc = Scorer(0)
+    sc.nccl_init(1, 0, nccl_unique_id())
+    bad = HostBatchArrays(b.turns, b.ids.copy(), b.lp, b.reward, b.usable, b.group_off)
+    bad.ids[3] = cfg.vocab + 7
+    with pytest.raises(RolloutError) as e:
+        sc.score_host(bad, cfg, pool, fill=True)
+    assert e.value.code == "shape_mismatch"
+    short = HostBatchArrays(b.turns, b.ids[:-1], b.lp[:-1], b.reward, b.usable, b.group_off)
+    with pytest.raises(RolloutError) as e:
+        sc.score_host(short, cfg, pool, fill=True)
+    assert e.value.code == "shape_mismatch"
+    # the communicator and the ctx stay usable; the flag is clear on success
+    got, _ = sc.score_host(b, cfg, pool, fill=True, seed=3)
+    assert got[N.P_ERR_RANKS] == 0.0 and got[N.P_N_ACTIVE] == sh.n_active
