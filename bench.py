@@ -176,6 +176,56 @@ def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
             "frac_of_nominal_8000": gbs / 8000.0}
 
 
+def measure_train_step(sc, pool, c, args, reps: int = 10) -> dict:
+    """K7 (one-pass training step: logprob/entropy + loss partials + dL/dlogits
+    from ONE read of each logits row, thread-block clusters) on one full logits
+    micro-batch, beside the two-pass K2+K4 -> K5 sequence it replaces. Reads
+    pool[0], writes the bf16 gradient into pool[1]."""
+    import torch
+    from paper_2603_18815_b200 import _native as N
+    n, V = pool[0].shape
+    g = torch.Generator(device="cuda").manual_seed(7)
+    targets = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
+    logp, _ = sc.logprob_entropy(pool[0], targets)
+    old = logp + 0.3 * (torch.rand(n, device="cuda", generator=g) - 0.5)
+    adv = torch.randn(64, device="cuda", generator=g)
+    seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
+    turn = torch.randint(0, 30, (n,), device="cuda", dtype=torch.int16, generator=g)
+    part = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device="cuda")
+    lp = torch.empty(n, dtype=torch.float32, device="cuda")
+
+    def one_pass():
+        sc.score_grad(pool[0], targets, old, adv, seq, turn, float(n), grad=pool[1], partials=part, want_rows=False)
+
+    def two_pass():
+        _, lp2, _ = sc.score_rows(pool[0], targets, old, adv, seq, turn, partials=part)
+        sc.logits_grad(pool[0], targets, lp2, old, adv, seq, float(n), grad=pool[1])
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    ms1 = timed(one_pass)
+    ms2 = timed(two_pass)
+    esz = 2 if c["dtype"] == "bf16" else 4
+    bpr = 2 * V * esz + 30  # read the row + write its gradient; target, old, adv, seq, turn, row bookkeeping
+    gbs = n * bpr / (ms1 / 1e3) / 1e9
+    peak, kind = measured_peak_gbs()
+    return {"kernel": "k_train (K7: K2+K4+K5 in one HBM pass, clusters of %d CTAs per row)"
+                      % sc.score_grad_cluster(pool[0], grad=pool[1]),
+            "rows_per_launch": n, "ms_per_launch": ms1, "rows_per_s": n / (ms1 / 1e3), "bytes_per_row": bpr,
+            "achieved_gbs": gbs, "frac_of_measured": gbs / peak, "frac_of_nominal_8000": gbs / 8000.0,
+            "two_pass_k2k4_k5_ms": ms2, "speedup_vs_two_pass": ms2 / ms1}
+
+
 def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
     """K6 (fused LM head + logprob, SURVEY §8 f rank 2) at the Qwen3-4B LM-head
     shape (d = 2560, V = config vocab): tcgen05 GEMM with the online-softmax
@@ -381,6 +431,12 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and not args.no_backward else None
+    train_step = None
+    if args.pool >= 2 and not args.no_backward:
+        try:
+            train_step = measure_train_step(sc, pool, c, args)
+        except Exception as ex:
+            train_step = {"error": repr(ex)}
     lmhead = measure_lmhead(sc, c, args) if not args.no_backward and c["dtype"] == "bf16" else None
     lmhead_step = None
     if lmhead is not None:
@@ -453,6 +509,7 @@ def run_ours(args):
                        "clip_hi_frac": res["clip_hi_frac"], "n_active": res["n_active"]},
             "cpu_baseline": cpu,
             "backward": backward,
+            "train_step": train_step,
             "lmhead": lmhead,
             "lmhead_step": lmhead_step,
             "ingest": ingest,

@@ -196,6 +196,28 @@ int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
                       float* dlogp, void* stream);
 
+/* ---- K7: the training step over the logits in one HBM pass --------------------- */
+/* prorl_score_rows + prorl_logits_grad from a single read of each logits row:
+ * logp / entropy (optional outputs), the loss partials added into
+ * partials_dev[PRORL_N_PARTIALS] (as prorl_score_rows) and grad (as
+ * prorl_logits_grad, with the row's lse from this same pass; grad may alias
+ * logits). Runs on thread-block clusters that keep each row in shared memory
+ * between the statistics and the gradient phase (4V bytes per bf16 row instead
+ * of 2V + 4V). Needs 16-B aligned logits/grad rows (base and row stride);
+ * other layouts run K2+K4 then K5 (same results within the stated
+ * tolerances). grad_stride must equal row_stride. */
+int prorl_score_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
+                     const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                     const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
+                     float inv_temp, const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy,
+                     double* partials_dev, void* grad, int64_t grad_stride, float* dlogp, void* stream);
+/* Cluster size (CTAs per row) prorl_score_grad uses for this layout; 0 = the
+ * two-pass K2+K5 path. */
+int prorl_score_grad_cluster(int dtype, int32_t vocab, int64_t row_stride, const void* logits, const void* grad);
+/* Co-resident clusters of `cluster` CTAs the K7 kernel fits on the current
+ * device (0: that cluster size cannot launch). */
+int prorl_score_grad_capacity(int cluster);
+
 /* ---- K6: fused LM head + logprob / entropy (SURVEY §8 f rank 2) ------------- */
 /* logits_i = W . h_i (bf16 hidden [n_rows x d], row stride h_stride; bf16
  * LM-head weight [V x d], row stride w_stride; d % 64 == 0, 16-B aligned

@@ -249,21 +249,27 @@ void oracle_row_logprob(const void* row, int dtype, int32_t vocab, int32_t targe
                         double* entropy) {
   const double it = (double)inv_temp;
   double m = -INFINITY;
+  int32_t vmax = 0;
   for (int32_t v = 0; v < vocab; ++v) {
     double x = logit_at(row, dtype, v) * it;
-    if (x > m) m = x;
+    if (x > m) {
+      m = x;
+      vmax = v;
+    }
   }
-  double S = 0.0, T = 0.0;
+  /* S = 1 + S_rest with the (first) maximum kept out of S_rest, so that
+   * ln S = log1p(S_rest) keeps full relative precision when p_max -> 1 */
+  double Sr = 0.0, T = 0.0;
   for (int32_t v = 0; v < vocab; ++v) {
     double x = logit_at(row, dtype, v) * it;
-    if (x == -INFINITY) continue;
+    if (x == -INFINITY || v == vmax) continue;
     double e = exp(x - m);
-    S += e;
+    Sr += e;
     T += (x - m) * e;
   }
-  const double lnS = log(S);
+  const double lnS = log1p(Sr);
   *logp = logit_at(row, dtype, target) * it - m - lnS;
-  *entropy = lnS - T / S;
+  *entropy = lnS - T / (1.0 + Sr);
 }
 
 void oracle_logprob_entropy(const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
@@ -346,7 +352,8 @@ void oracle_logits_grad(const void* logits, int dtype, int64_t row_stride, int32
     for (int32_t v = 0; v < vocab; ++v) {
       const double x = logit_at(row, dtype, v) * it;
       const double pv = x == -INFINITY ? 0.0 : exp(x - lse);
-      gr[v] = g * it * ((v == targets[i] ? 1.0 : 0.0) - pv);
+      /* 1 - p_y = -expm1(logp): exact as p_y -> 1 */
+      gr[v] = v == targets[i] ? -g * it * expm1(lp) : -g * it * pv;
     }
   }
 }

@@ -20,13 +20,14 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "rowmath.cuh"
 #include "stream.cuh"
 
 namespace prorl {
 
 namespace {
 
-constexpr float kLog2e = 1.44269504088896340736f;
+using namespace rowmath;
 
 struct GradArgs {
   const uint8_t* logits;
@@ -47,43 +48,6 @@ struct GradArgs {
   float lo, hi;    // 1 - eps_lo, 1 + eps_hi
   float inv_n;     // 1 / N_global
   float* dlogp;    // optional per-row dL/dlogp
-};
-
-template <typename T> struct GElem;
-template <> struct GElem<__nv_bfloat16> {
-  static constexpr int ES = 2;
-  __device__ static float load(const uint8_t* row, int64_t i) {
-    return __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(row) + i)) << 16);
-  }
-  __device__ static void store(uint8_t* row, int64_t i, float g) {
-    reinterpret_cast<__nv_bfloat16*>(row)[i] = __float2bfloat16_rn(g);
-  }
-  // 8 logits in, 8 gradients out (scale s = -dL/dlogp * inv_T, base-2 lse l2)
-  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
-      const float2 d = __ffma2_rn(x, c2, nl2);
-      const float2 p = make_float2(ex2_approx(d.x), ex2_approx(d.y));
-      const float2 g = __fmul2_rn(p, s2);
-      const __nv_bfloat162 b = __float22bfloat162_rn(g);
-      w[q] = *reinterpret_cast<const uint32_t*>(&b);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-  }
-};
-template <> struct GElem<float> {
-  static constexpr int ES = 4;
-  __device__ static float load(const uint8_t* row, int64_t i) { return __ldg(reinterpret_cast<const float*>(row) + i); }
-  __device__ static void store(uint8_t* row, int64_t i, float g) { reinterpret_cast<float*>(row)[i] = g; }
-  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
-    const float2 da = __ffma2_rn(make_float2(__uint_as_float(v.x), __uint_as_float(v.y)), c2, nl2);
-    const float2 db = __ffma2_rn(make_float2(__uint_as_float(v.z), __uint_as_float(v.w)), c2, nl2);
-    const float2 ga = __fmul2_rn(make_float2(ex2_approx(da.x), ex2_approx(da.y)), s2);
-    const float2 gb = __fmul2_rn(make_float2(ex2_approx(db.x), ex2_approx(db.y)), s2);
-    return make_uint4(__float_as_uint(ga.x), __float_as_uint(ga.y), __float_as_uint(gb.x), __float_as_uint(gb.y));
-  }
 };
 
 template <typename T, int WARPS, int STAGES, int CHUNK>
@@ -109,9 +73,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
     const int tail = (int)((reinterpret_cast<uintptr_t>(rp) + (uintptr_t)p.vocab * ES - b) / ES);
     const int32_t y = p.targets[i];
     // per-row scale (lane 0), broadcast
-    float s = 0.f, l2 = 0.f, xy = 0.f;
+    float s = 0.f, l2 = 0.f, gy = 0.f;
     if (lane == 0) {
-      xy = GElem<T>::load(rp, y);
+      const float xy = GElem<T>::load(rp, y);
       const float lp = p.logp[i], old = p.old_lp[i];
       const float A = p.adv[p.row_seq[i]];
       const float ratio = expf(lp - old);
@@ -121,10 +85,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
       if (p.dlogp) p.dlogp[i] = dl;
       s = -dl * p.inv_temp;  // grad_v = s * p_v for v != y, grad_y = -s * (1 - p_y)
       l2 = fmaf(xy, p.c, -lp * kLog2e);                            // lse in base-2 units
+      gy = s * expm1f(lp);  // -s (1 - p_y), exact as p_y -> 1
     }
     s = __shfl_sync(0xffffffffu, s, 0);
     l2 = __shfl_sync(0xffffffffu, l2, 0);
-    xy = __shfl_sync(0xffffffffu, xy, 0);
     const float2 c2 = make_float2(p.c, p.c), nl2 = make_float2(-l2, -l2), s2 = make_float2(s, s);
     const bool zero = (s == 0.f);  // warp-uniform: clipped branch / A == 0 -> all-zero row
 
@@ -155,10 +119,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
       }
     }
     __syncwarp();  // order the row's vector stores before the target fix-up
-    if (lane == 0) {
-      const float py = ex2_approx(fmaf(xy, p.c, -l2));
-      GElem<T>::store(gp, y, -s * (1.f - py));
-    }
+    if (lane == 0) GElem<T>::store(gp, y, gy);
   }
 }
 

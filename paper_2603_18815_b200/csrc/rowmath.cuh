@@ -1,0 +1,236 @@
+// rowmath.cuh — per-row arithmetic shared by the logits-streaming kernels
+// (K2 score.cu, K5 grad.cu, K7 train.cu): element loaders, the warp-uniform
+// running max with top-element exclusion, the DAPO per-row loss and the
+// gradient vector maths. Definitions: SURVEY.md App. B.2-B.5.
+#pragma once
+
+#include "common.cuh"
+
+namespace prorl {
+namespace rowmath {
+
+constexpr float kLog2e = 1.44269504088896340736f;
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T> struct Elem;
+
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int kSize = 2;
+  static constexpr uint32_t kClampWord = 0xf000f000u;  // two bf16 -2^97 (the clamp floor)
+  __device__ static float load(const uint8_t* row, int64_t idx) {
+    uint32_t b = __ldg(reinterpret_cast<const unsigned short*>(row) + idx);
+    b = b > 0xf000u ? 0xf000u : b;  // same clamp as the packed path
+    return __uint_as_float(b << 16);
+  }
+  // Group max (packed HMNMX2). The fast path runs unclamped: a -inf / NaN
+  // logit turns the row's T sum into NaN, which sends the row down the
+  // clamped re-read path (row_slow) instead of paying a clamp per logit.
+  template <int NV>
+  __device__ static float group_max(uint4 (&v)[NV]) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      __nv_bfloat162 a = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].x), *reinterpret_cast<__nv_bfloat162*>(&v[j].y));
+      __nv_bfloat162 b = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v[j].z), *reinterpret_cast<__nv_bfloat162*>(&v[j].w));
+      a = __hmax2(a, b);
+      if (j == 0) m = *reinterpret_cast<uint32_t*>(&a);
+      else {
+        __nv_bfloat162 mm = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&m), a);
+        m = *reinterpret_cast<uint32_t*>(&mm);
+      }
+    }
+    return fmaxf(__uint_as_float(m << 16), __uint_as_float(m & 0xffff0000u));
+  }
+  template <int NV>
+  __device__ static void mask_first(uint4 (&v)[NV], float top) {
+    const uint32_t tb = __float_as_uint(top) >> 16;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      uint32_t* w = &v[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!done && (w[q] & 0xffffu) == tb) {
+          w[q] = (w[q] & 0xffff0000u) | 0xf000u;
+          done = true;
+        }
+        if (!done && (w[q] >> 16) == tb) {
+          w[q] = (w[q] & 0xffffu) | 0xf0000000u;
+          done = true;
+        }
+      }
+    }
+  }
+  // Two logits per step on the packed fp32x2 pipe (FFMA2 / FADD2, sm_100):
+  // d = x*c - M, e = 2^d (two MUFU.EX2), S += e, T += d*e.
+  template <int NV>
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+        const float2 d = __ffma2_rn(x, c2, nM2);
+        const float2 e = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+        S[q & 1] = __fadd2_rn(S[q & 1], e);
+        Tt[q & 1] = __ffma2_rn(d, e, Tt[q & 1]);
+      }
+    }
+  }
+};
+
+template <> struct Elem<float> {
+  static constexpr int kSize = 4;
+  static constexpr float kFloor = -1.5845632502852868e29f;  // -2^97, same floor as bf16
+  static constexpr uint32_t kClampWord = 0xf0000000u;       // bits of -2^97
+  __device__ static float load(const uint8_t* row, int64_t idx) {
+    return fmaxf(__ldg(reinterpret_cast<const float*>(row) + idx), kFloor);
+  }
+  template <int NV>
+  __device__ static float group_max(uint4 (&v)[NV]) {
+    float m = kFloor;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      m = fmaxf(m, fmaxf(fmaxf(__uint_as_float(v[j].x), __uint_as_float(v[j].y)),
+                         fmaxf(__uint_as_float(v[j].z), __uint_as_float(v[j].w))));
+    return m;
+  }
+  template <int NV>
+  __device__ static void mask_first(uint4 (&v)[NV], float top) {
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      uint32_t* w = &v[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!done && __uint_as_float(w[q]) == top) {
+          w[q] = kClampWord;
+          done = true;
+        }
+    }
+  }
+  template <int NV>
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const float2 xa = make_float2(__uint_as_float(v[j].x), __uint_as_float(v[j].y));
+      const float2 xb = make_float2(__uint_as_float(v[j].z), __uint_as_float(v[j].w));
+      const float2 da = __ffma2_rn(xa, c2, nM2), db = __ffma2_rn(xb, c2, nM2);
+      const float2 ea = make_float2(ex2_approx(da.x), ex2_approx(da.y));
+      const float2 eb = make_float2(ex2_approx(db.x), ex2_approx(db.y));
+      S[0] = __fadd2_rn(S[0], ea);
+      Tt[0] = __ffma2_rn(da, ea, Tt[0]);
+      S[1] = __fadd2_rn(S[1], eb);
+      Tt[1] = __ffma2_rn(db, eb, Tt[1]);
+    }
+  }
+};
+
+// Warp-uniform running maximum and the excluded top element.
+struct Top {
+  float Mc;  // running max of x*c (rounded), -inf before the first element
+  float Mx;  // the raw (clamped) logit that set it
+};
+
+// Called by the whole warp when some lane saw lm*c > Mc. Rescales every
+// lane's sums to the new max, turns the previous top element into an ordinary
+// term (added by lane 0), and returns the lane that holds the new top element
+// (lowest lane on ties) — that lane must exclude one copy of it from its sums.
+__device__ __forceinline__ int raise_top(float lm, float c, Top& top, float2 (&S)[2], float2 (&Tt)[2], int lane) {
+  const float gl = warp_max(lm);
+  const float nMc = gl * c;
+  if (top.Mc != -INFINITY) {
+    const float sc = ex2_approx(top.Mc - nMc);
+    const float dl = nMc - top.Mc;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      Tt[k].x = sc * fmaf(-dl, S[k].x, Tt[k].x);
+      Tt[k].y = sc * fmaf(-dl, S[k].y, Tt[k].y);
+      S[k].x *= sc;
+      S[k].y *= sc;
+    }
+    if (lane == 0) {
+      const float d = fmaf(top.Mx, c, -nMc);
+      const float e = ex2_approx(d);
+      S[0].x += e;
+      Tt[0].x = fmaf(d, e, Tt[0].x);
+    }
+  }
+  top.Mc = nMc;
+  top.Mx = gl;
+  return __ffs(__ballot_sync(kFull, lm == gl)) - 1;
+}
+
+// k3 KL estimator e^d - d - 1 (d = ref - logp), accurate for small |d|.
+__device__ __forceinline__ float kl_k3(float d) {
+  if (fabsf(d) < 0.125f) return d * d * fmaf(d, fmaf(d, fmaf(d, 1.f / 120.f, 1.f / 24.f), 1.f / 6.f), 0.5f);
+  return expm1f(d) - d;
+}
+
+// Per-row loss terms (App. B.4/B.5 + optional KL), fp32 math.
+struct RowLoss {
+  float loss, ratio, clip_lo, clip_hi, kl;
+};
+__device__ __forceinline__ RowLoss row_loss(float logp, float old, float A, float lo, float hi, const float* ref,
+                                            int64_t i, float kl_coef) {
+  RowLoss r;
+  r.ratio = expf(logp - old);
+  const float pg1 = r.ratio * A;
+  const float pg2 = fminf(fmaxf(r.ratio, lo), hi) * A;
+  r.loss = -fminf(pg1, pg2);
+  r.clip_lo = (r.ratio < lo && A < 0.f) ? 1.f : 0.f;
+  r.clip_hi = (r.ratio > hi && A > 0.f) ? 1.f : 0.f;
+  r.kl = 0.f;
+  if (ref) {
+    r.kl = kl_k3(ref[i] - logp);
+    r.loss = fmaf(kl_coef, r.kl, r.loss);
+  }
+  return r;
+}
+
+// per-row global sums kept by the loss epilogue; index = partials index
+// (8, 9 belong to K3 and stay 0 here; 10 = sum k3 KL)
+constexpr int kNG = 11;
+constexpr int kBucketDoubles = PRORL_TURN_BUCKETS * PRORL_N_PER_TURN;
+
+template <typename T> struct GElem;
+template <> struct GElem<__nv_bfloat16> {
+  static constexpr int ES = 2;
+  __device__ static float load(const uint8_t* row, int64_t i) {
+    return __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(row) + i)) << 16);
+  }
+  __device__ static void store(uint8_t* row, int64_t i, float g) {
+    reinterpret_cast<__nv_bfloat16*>(row)[i] = __float2bfloat16_rn(g);
+  }
+  // 8 logits in, 8 gradients out (scale s = -dL/dlogp * inv_T, base-2 lse l2)
+  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+      const float2 d = __ffma2_rn(x, c2, nl2);
+      const float2 p = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+      const float2 g = __fmul2_rn(p, s2);
+      const __nv_bfloat162 b = __float22bfloat162_rn(g);
+      w[q] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <> struct GElem<float> {
+  static constexpr int ES = 4;
+  __device__ static float load(const uint8_t* row, int64_t i) { return __ldg(reinterpret_cast<const float*>(row) + i); }
+  __device__ static void store(uint8_t* row, int64_t i, float g) { reinterpret_cast<float*>(row)[i] = g; }
+  __device__ static uint4 vec(uint4 v, float2 c2, float2 nl2, float2 s2) {
+    const float2 da = __ffma2_rn(make_float2(__uint_as_float(v.x), __uint_as_float(v.y)), c2, nl2);
+    const float2 db = __ffma2_rn(make_float2(__uint_as_float(v.z), __uint_as_float(v.w)), c2, nl2);
+    const float2 ga = __fmul2_rn(make_float2(ex2_approx(da.x), ex2_approx(da.y)), s2);
+    const float2 gb = __fmul2_rn(make_float2(ex2_approx(db.x), ex2_approx(db.y)), s2);
+    return make_uint4(__float_as_uint(ga.x), __float_as_uint(ga.y), __float_as_uint(gb.x), __float_as_uint(gb.y));
+  }
+};
+
+}  // namespace rowmath
+}  // namespace prorl

@@ -167,6 +167,36 @@ class Scorer:
                                       _stream(stream)))
         return grad, dl
 
+    # ---- K7: one-pass training step (K2 + K4 + K5 from one read of each row) ----
+    def score_grad(self, logits, targets, old_lp, adv, row_seq, row_turn, n_global: float, rows=None,
+                   inv_temp: float = 1.0, cfg: LossConfig | None = None, grad=None, partials=None,
+                   want_rows: bool = True, want_dlogp: bool = False, vocab: int | None = None, ref_lp=None,
+                   stream=None):
+        """(partials, logp, entropy, grad, dlogp): score_rows + logits_grad in one HBM pass per row."""
+        n = targets.numel()
+        dev = targets.device
+        if partials is None:
+            partials = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=dev)
+        if grad is None:
+            grad = torch.empty_like(logits)
+        logp = torch.empty(n, dtype=torch.float32, device=dev) if want_rows else None
+        ent = torch.empty(n, dtype=torch.float32, device=dev) if want_rows else None
+        dl = torch.empty(n, dtype=torch.float32, device=dev) if want_dlogp else None
+        c = (cfg or LossConfig()).c()
+        V = vocab if vocab is not None else logits.shape[1]
+        check(N.lib.prorl_score_grad(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
+                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
+                                     inv_temp, C.byref(c), float(n_global), ptr(logp), ptr(ent), ptr(partials),
+                                     ptr(grad), grad.stride(0), ptr(dl), _stream(stream)))
+        return partials, logp, ent, grad, dl
+
+    @staticmethod
+    def score_grad_cluster(logits: torch.Tensor, vocab: int | None = None, grad=None) -> int:
+        """CTAs per row the one-pass kernel uses for this layout (0 = two-pass K2+K5 path)."""
+        V = vocab if vocab is not None else logits.shape[1]
+        return N.lib.prorl_score_grad_cluster(_DT[logits.dtype], V, logits.stride(0), ptr(logits),
+                                              ptr(grad if grad is not None else logits))
+
     # ---- K6: fused LM head (tcgen05) ----
     def lmhead_logprob(self, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor,
                        inv_temp: float = 1.0, stream=None):

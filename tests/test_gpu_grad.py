@@ -114,3 +114,21 @@ def test_logits_grad_layout_errors(scorer, cuda):
     bad = torch.zeros((4, 72), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(RolloutError):
         scorer.logits_grad(x, t, f, f, f, t, 10.0, grad=bad)
+
+
+def test_logits_grad_dominant_and_masked_rows(scorer, cuda):
+    """p_y -> 1 (the target gradient -g (1 - p_y) must not pick up the fp32
+    rounding of the lse) and -inf (masked) logits."""
+    V, n = 32000, 4
+    rng = np.random.default_rng(8)
+    xh = rng.normal(0, 2, (n, V)).astype(np.float32)
+    xh[0, 77] = 60.0
+    xh[1, ::5] = -np.inf
+    xh[2] = 0.25
+    t = np.array([77, 3, 9, 11], np.int32)
+    x = torch.from_numpy(xh).to(cuda).to(torch.bfloat16)
+    host = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    old = np.full(n, -0.7, np.float32)
+    adv = np.array([1.0, -1.0], np.float32)
+    seq = np.array([0, 1, 0, 1], np.int32)
+    _check(scorer, cuda, x, host, t, old, adv, seq, V, "bf16", n_global=10.0)

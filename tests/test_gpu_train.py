@@ -1,0 +1,189 @@
+"""K7 (one-pass training step: logprob/entropy + DAPO loss partials + dL/dlogits
+from a single read of each logits row, on thread-block clusters) vs the fp64
+oracle, and vs the two-pass K2+K4 -> K5 path it replaces.
+
+Tolerances as the kernels it fuses: logp/entropy |g - o| <= 1e-5 max(|o|, 1e-3);
+partial sums <= 1e-5 of the sum's condition scale, counts exact except rows
+within 1e-5 of a clip bound; dL/dlogp 1e-5 relative; gradient elements one
+bf16 rounding (2^-8 relative) for bf16, 1e-5 relative for fp32. Rows whose
+clip decision is within 1e-5 of flipping (oracle `border`) are skipped for
+the gradient."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2603_18815_b200 import _native as N
+from paper_2603_18815_b200.hotpath import LossConfig, Scorer
+from tests.test_gpu_parity import assert_partials_close, assert_rows_close
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, d):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(d)
+
+
+def _case(scorer, cuda, V, n, dtype, stride=None, seed=0, n_seq=11):
+    rng = np.random.default_rng(seed)
+    targets = rng.integers(0, V, n).astype(np.int32)
+    old = (-0.05 - 2.95 * rng.random(n)).astype(np.float32)
+    stride = stride or V
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = torch.empty((n, stride), dtype=tdt, device=cuda)
+    scorer.gen_logits(x, n, 1000, dev(targets, cuda), dev(old, cuda), seed=seed + 5, sigma=2.0, vocab=V)
+    host = O.gen_logits(n, V, 1000, targets, old, seed=seed + 5, sigma=2.0, dtype=dtype, row_stride=stride)
+    adv = rng.normal(0, 1, n_seq).astype(np.float32)
+    seq = rng.integers(0, n_seq, n).astype(np.int32)
+    turn = rng.integers(-1, 70, n).astype(np.int16)
+    return x, host, targets, old, adv, seq, turn
+
+
+def _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, n_global, rows=None, cfg=None, ref=None,
+               inplace=False):
+    kl = cfg.kl_coef if cfg else 0.0
+    rd = None if rows is None else dev(rows, cuda)
+    part, lp, ent, g, dl = scorer.score_grad(x, dev(t, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
+                                             dev(turn, cuda), n_global, rows=rd, cfg=cfg, vocab=V,
+                                             grad=x if inplace else None, want_dlogp=True,
+                                             ref_lp=None if ref is None else dev(ref, cuda))
+    torch.cuda.synchronize()
+    olp, oent = O.logprob_entropy(host, t, rows=rows, vocab=V)
+    assert_rows_close(lp.cpu().numpy(), olp, "logp")
+    assert_rows_close(ent.cpu().numpy(), oent, "entropy")
+    P, Q, nb = O.loss(olp, oent, old, adv.astype(np.float64), seq, turn, ref_lp=ref, kl_coef=kl)
+    assert_partials_close(part.cpu().numpy(), P, Q, nb, "k7")
+    og, odl, bd = O.logits_grad(host, t, old, adv.astype(np.float64), seq, n_global, rows=rows, vocab=V,
+                                ref_lp=ref, kl_coef=kl)
+    ok = bd == 0
+    assert ok.sum() > 0.9 * len(ok)
+    d = dl.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(d[ok] - odl[ok]) <= 1e-5 * np.abs(odl[ok]) + 1e-12)
+    r = np.arange(len(t)) if rows is None else rows
+    got = g.float().cpu().numpy()[r, :V].astype(np.float64)
+    tol = (2.0 ** -8 if dtype == "bf16" else 1e-5) * np.abs(og) + 1e-30
+    bad = (np.abs(got - og) > tol) & ok[:, None]
+    assert not bad.any(), (np.argwhere(bad)[:5], got[bad][:5], og[bad][:5])
+    return part, lp, ent, g, dl
+
+
+@pytest.mark.parametrize("dtype,V,stride,n,cluster", [
+    ("bf16", 32000, None, 300, (1, 1)),
+    ("bf16", 151936, None, 64, (2, 4)),
+    ("bf16", 262144, None, 20, (6, 8)),
+    ("fp32", 151936, None, 16, (6, 8)),
+    ("fp32", 32000, None, 90, (2, 4)),
+    ("bf16", 1003, 1008, 200, (1, 1)),    # 3-element tail after the 16-B interior
+    ("fp32", 4099, 4100, 60, (1, 1)),     # 3-element tail, fp32
+    ("bf16", 7, 8, 40, (1, 1)),           # no interior at all: the whole row is tail
+    ("bf16", 1003, None, 120, (0, 0)),    # unaligned row stride: two-pass K2+K5 path
+    ("bf16", 600000, None, 3, (0, 0)),    # row too large for 8 CTAs: two-pass path
+])
+def test_score_grad_vs_oracle(scorer, cuda, dtype, V, stride, n, cluster):
+    x, host, t, old, adv, seq, turn = _case(scorer, cuda, V, n, dtype, stride=stride, seed=V % 89 + n)
+    cs = Scorer.score_grad_cluster(x, vocab=V)
+    assert cluster[0] <= cs <= cluster[1], cs
+    _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, n_global=5000.0)
+
+
+def test_score_grad_matches_two_pass(scorer, cuda):
+    """K7 == K2+K4 then K5 on the same rows, within the kernels' tolerances."""
+    V, n = 151936, 512
+    x, host, t, old, adv, seq, turn = _case(scorer, cuda, V, n, "bf16", seed=7)
+    td, od, ad, sd, trd = (dev(a, cuda) for a in (t, old, adv, seq, turn))
+    p1, lp1, ent1, g1, dl1 = scorer.score_grad(x, td, od, ad, sd, trd, 904452.0, want_dlogp=True)
+    p2, lp2, ent2 = scorer.score_rows(x, td, od, ad, sd, trd)
+    g2, dl2 = scorer.logits_grad(x, td, lp2, od, ad, sd, 904452.0, want_dlogp=True)
+    torch.cuda.synchronize()
+    a, b = lp1.double().cpu().numpy(), lp2.double().cpu().numpy()
+    assert np.all(np.abs(a - b) <= 2e-5 * np.maximum(np.abs(b), 1e-3))
+    a, b = ent1.double().cpu().numpy(), ent2.double().cpu().numpy()
+    assert np.all(np.abs(a - b) <= 2e-5 * np.maximum(np.abs(b), 1e-3))
+    P1, P2 = p1.cpu().numpy(), p2.cpu().numpy()
+    assert P1[N.P_N_ACTIVE] == P2[N.P_N_ACTIVE] == n
+    assert abs(P1[N.P_LOSS_SUM] - P2[N.P_LOSS_SUM]) <= 1e-5 * np.abs(P2[N.P_LOSS_SUM]) + 1e-6
+    # gradients: same rows zero (clip decisions agree away from the border), values within 2 bf16 ulps
+    G1, G2 = g1.float().cpu().numpy(), g2.float().cpu().numpy()
+    assert np.all(np.abs(G1 - G2) <= 2.0 ** -7 * np.maximum(np.abs(G1), np.abs(G2)) + 1e-30)
+
+
+def test_score_grad_rows_inplace_deterministic(scorer, cuda):
+    V, n = 151936, 96
+    x, host, t, old, adv, seq, turn = _case(scorer, cuda, V, n, "bf16", seed=11)
+    rows = np.random.default_rng(2).permutation(n).astype(np.int32)
+    x0 = x.clone()
+    part, lp, ent, g, dl = _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 333.0, rows=rows)
+    # bit-identical on a second run (fixed reduction order, no atomics)
+    part2, lp2, ent2, g2, dl2 = scorer.score_grad(x, dev(t, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
+                                                  dev(turn, cuda), 333.0, rows=dev(rows, cuda), want_dlogp=True)
+    assert torch.equal(part, part2) and torch.equal(lp, lp2) and torch.equal(g, g2)
+    # in place: the gradient overwrites the logits and equals the out-of-place result
+    xi = x0.clone()
+    part3, lp3, *_ = scorer.score_grad(xi, dev(t, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
+                                       dev(turn, cuda), 333.0, rows=dev(rows, cuda), grad=xi)
+    torch.cuda.synchronize()
+    assert torch.equal(xi, g) and torch.equal(part3, part) and torch.equal(lp3, lp)
+
+
+def test_score_grad_kl_and_zero_advantage(scorer, cuda):
+    V, n = 65536, 128
+    x, host, t, old, adv, seq, turn = _case(scorer, cuda, V, n, "bf16", seed=21, n_seq=8)
+    adv[3] = 0.0  # rows of sequence 3 have a zero gradient without the KL term
+    lp0, _ = scorer.logprob_entropy(x, dev(t, cuda))
+    ref = (lp0.cpu().numpy() + np.random.default_rng(3).normal(0, 0.4, n)).astype(np.float32)
+    _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 300.0, cfg=LossConfig(kl_coef=0.25),
+               ref=ref)
+    part, lp, ent, g, dl = scorer.score_grad(x, dev(t, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
+                                             dev(turn, cuda), 300.0, want_dlogp=True)
+    z = seq == 3
+    assert z.any() and torch.count_nonzero(g[torch.from_numpy(z).to(cuda)]).item() == 0
+
+
+def test_score_grad_edge_rows(scorer, cuda):
+    """All-equal logits (H = ln V), one dominant logit (p -> 1), -inf entries,
+    ties at the maximum across the two CTAs of a cluster."""
+    V, n = 151936, 6
+    rng = np.random.default_rng(5)
+    xh = rng.normal(0, 2, (n, V)).astype(np.float32)
+    xh[0] = 0.5
+    xh[1, 1234] = 60.0
+    xh[2, ::3] = -np.inf
+    xh[3, 17] = xh[3, V - 17] = 30.0   # equal maxima in both halves of the row
+    xh[4, V // 2] = 25.0              # max at the slice boundary
+    t = np.array([5, 1234, 4, V - 17, V // 2, 9], np.int32)
+    x = torch.from_numpy(xh).to(cuda).to(torch.bfloat16)
+    host = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    old = np.full(n, -0.7, np.float32)
+    adv = np.array([1.0, -1.0], np.float32)
+    seq = np.array([0, 1, 0, 1, 0, 1], np.int32)
+    turn = np.zeros(n, np.int16)
+    part, lp, ent, g, dl = _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 10.0)
+    e = ent.cpu().numpy()
+    assert abs(e[0] - np.log(V)) < 1e-4 and e[1] < 1e-6
+    assert torch.isfinite(g.float()).all()
+
+
+def test_score_grad_full_microbatch_properties(scorer, cuda):
+    """A full C2 micro-batch (16 576 rows x 151 936): partials equal the fused
+    K2+K4 pass, every gradient row sums to ~0 and is finite."""
+    V, n = 151936, 16576
+    rng = np.random.default_rng(31)
+    t = rng.integers(0, V, n).astype(np.int32)
+    old = (-0.05 - 2.95 * rng.random(n)).astype(np.float32)
+    x = torch.empty((n, V), dtype=torch.bfloat16, device=cuda)
+    scorer.gen_logits(x, n, 0, dev(t, cuda), dev(old, cuda), seed=9, sigma=2.0)
+    adv = rng.normal(0, 1, 280).astype(np.float32)
+    seq = np.sort(rng.integers(0, 280, n)).astype(np.int32)
+    turn = rng.integers(0, 40, n).astype(np.int16)
+    td, od, ad, sd, trd = (dev(a, cuda) for a in (t, old, adv, seq, turn))
+    p2, lp2, _ = scorer.score_rows(x, td, od, ad, sd, trd)
+    p1, lp1, _, g, _ = scorer.score_grad(x, td, od, ad, sd, trd, float(n), grad=x)   # in place
+    torch.cuda.synchronize()
+    P1, P2 = p1.cpu().numpy(), p2.cpu().numpy()
+    assert P1[N.P_N_ACTIVE] == n
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM):
+        assert abs(P1[i] - P2[i]) <= 1e-5 * abs(P2[i]) + 1e-6, (i, P1[i], P2[i])
+    assert abs(P1[N.P_CLIP_LO] - P2[N.P_CLIP_LO]) <= 3
+    s = x.float().sum(dim=1)
+    mx = x.float().abs().amax(dim=1)
+    assert torch.isfinite(s).all() and bool((s.abs() <= V * 2.0 ** -8 * mx + 1e-12).all())
