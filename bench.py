@@ -219,8 +219,7 @@ def measure_train_step(sc, pool, c, args, reps: int = 10) -> dict:
     bpr = 2 * V * esz + 30  # read the row + write its gradient; target, old, adv, seq, turn, row bookkeeping
     gbs = n * bpr / (ms1 / 1e3) / 1e9
     peak, kind = measured_peak_gbs()
-    return {"kernel": "k_train (K7: K2+K4+K5 in one HBM pass, clusters of %d CTAs per row)"
-                      % sc.score_grad_cluster(pool[0], grad=pool[1]),
+    return {"kernel": "k_train (K7: K2+K4+K5, one HBM read + one HBM write per row; second pass from L2)",
             "rows_per_launch": n, "ms_per_launch": ms1, "rows_per_s": n / (ms1 / 1e3), "bytes_per_row": bpr,
             "achieved_gbs": gbs, "frac_of_measured": gbs / peak, "frac_of_nominal_8000": gbs / 8000.0,
             "two_pass_k2k4_k5_ms": ms2, "speedup_vs_two_pass": ms2 / ms1}

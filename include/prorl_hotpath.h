@@ -196,27 +196,20 @@ int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
                       float* dlogp, void* stream);
 
-/* ---- K7: the training step over the logits in one HBM pass --------------------- */
-/* prorl_score_rows + prorl_logits_grad from a single read of each logits row:
- * logp / entropy (optional outputs), the loss partials added into
+/* ---- K7: the training step over the logits, one HBM read + one HBM write ---- */
+/* prorl_score_rows + prorl_logits_grad in one kernel: logp / entropy
+ * (optional outputs), the loss partials added into
  * partials_dev[PRORL_N_PARTIALS] (as prorl_score_rows) and grad (as
- * prorl_logits_grad, with the row's lse from this same pass; grad may alias
- * logits). Runs on thread-block clusters that keep each row in shared memory
- * between the statistics and the gradient phase (4V bytes per bf16 row instead
- * of 2V + 4V). Needs 16-B aligned logits/grad rows (base and row stride);
- * other layouts run K2+K4 then K5 (same results within the stated
- * tolerances). grad_stride must equal row_stride. */
+ * prorl_logits_grad, with the row's lse from this same kernel). One CTA owns a
+ * row: pass A reads it from HBM (statistics), pass B re-reads it from L2 and
+ * writes the gradient — 4V bytes of HBM per bf16 row instead of 2V + 4V.
+ * Same layouts as prorl_logits_grad: grad_stride == row_stride, grad with
+ * the logits' 16-B phase, grad may alias logits (in place). */
 int prorl_score_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                      const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                      float inv_temp, const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy,
                      double* partials_dev, void* grad, int64_t grad_stride, float* dlogp, void* stream);
-/* Cluster size (CTAs per row) prorl_score_grad uses for this layout; 0 = the
- * two-pass K2+K5 path. */
-int prorl_score_grad_cluster(int dtype, int32_t vocab, int64_t row_stride, const void* logits, const void* grad);
-/* Co-resident clusters of `cluster` CTAs the K7 kernel fits on the current
- * device (0: that cluster size cannot launch). */
-int prorl_score_grad_capacity(int cluster);
 
 /* ---- K6: fused LM head + logprob / entropy (SURVEY §8 f rank 2) ------------- */
 /* logits_i = W . h_i (bf16 hidden [n_rows x d], row stride h_stride; bf16

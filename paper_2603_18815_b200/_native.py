@@ -31,7 +31,7 @@ EXPORTS = [
     "prorl_abi_version", "prorl_kernel_config", "prorl_last_error", "prorl_status_code", "prorl_ctx_create", "prorl_ctx_destroy",
     "prorl_check_errors", "prorl_pack", "prorl_grpo_adv", "prorl_logprob_entropy", "prorl_clipped_loss",
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
-    "prorl_gen_logits_keyed", "prorl_row_keys", "prorl_logits_grad", "prorl_score_grad", "prorl_score_grad_cluster", "prorl_score_grad_capacity", "prorl_lmhead_logprob", "prorl_ingest_responses", "prorl_ingest_free",
+    "prorl_gen_logits_keyed", "prorl_row_keys", "prorl_logits_grad", "prorl_score_grad", "prorl_lmhead_logprob", "prorl_ingest_responses", "prorl_ingest_free",
     "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host",
 ]
 
@@ -98,8 +98,6 @@ def _load() -> C.CDLL:
                                         C.POINTER(LossCfg), f64, vp, i64, vp, vp]),
         "prorl_score_grad": (C.c_int, [vp, vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, vp, i64, f32,
                                        C.POINTER(LossCfg), f64, vp, vp, vp, vp, i64, vp, vp]),
-        "prorl_score_grad_cluster": (C.c_int, [C.c_int, i32, i64, vp, vp]),
-        "prorl_score_grad_capacity": (C.c_int, [C.c_int]),
         "prorl_ingest_responses": (C.c_int, [vp, vp, vp, i32, f64, i32, C.POINTER(IngestResult)]),
         "prorl_ingest_free": (C.c_int, [C.POINTER(IngestResult)]),
         "prorl_lmhead_logprob": (C.c_int, [vp, vp, i64, vp, i64, i32, i32, vp, i64, f32, vp, vp, vp]),

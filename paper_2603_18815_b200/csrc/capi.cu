@@ -255,13 +255,6 @@ int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_s
                      inv_temp, cfg, n_global, grad, grad_stride, dlogp, S(stream));
 }
 
-int prorl_score_grad_cluster(int dtype, int32_t vocab, int64_t row_stride, const void* logits, const void* grad) {
-  if ((dtype != PRORL_BF16 && dtype != PRORL_FP32) || vocab <= 0 || row_stride < vocab) return 0;
-  return train_cluster_size(dtype, vocab, row_stride, logits, grad ? grad : logits);
-}
-
-int prorl_score_grad_capacity(int cluster) { return train_max_clusters(cluster); }
-
 int prorl_score_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                      const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
@@ -275,29 +268,19 @@ int prorl_score_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_st
   if (!(inv_temp > 0.f) || !(n_global > 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "score_grad: bad inv_temp/n_global");
   if (cfg->n_buckets < 1 || cfg->n_buckets > PRORL_TURN_BUCKETS)
     return fail(PRORL_E_SHAPE, "score_grad: n_buckets out of [1, 64]");
+  const int esz = dtype == PRORL_BF16 ? 2 : 4;
+  const intptr_t delta = static_cast<const uint8_t*>(grad) - static_cast<const uint8_t*>(logits);
+  if (reinterpret_cast<uintptr_t>(logits) % esz || (delta % 16) != 0)
+    return fail(PRORL_E_SHAPE, "score_grad: grad must have the logits' 16-byte alignment phase");
   PRORL_CUDA(cudaSetDevice(c->device));
   if (n_rows <= 0) return PRORL_OK;
-  const int slab_rows = std::max(std::max(score_slab_rows(c), loss_slab_rows(c)), train_slab_rows(c));
-  PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)slab_rows));
+  const int slab_rows = train_slab_rows(c);
+  PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(slab_rows, loss_slab_rows(c))));
   int used = 0;
-  if (train_cluster_size(dtype, vocab, row_stride, logits, grad) > 0) {
-    PRORL_TRY(launch_train(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, ref_lp,
-                           n_rows, inv_temp, cfg, n_global, logp, entropy, dlogp, grad, c->slab.as<double>(), false,
-                           &used, S(stream)));
-    return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
-  }
-  // two-pass layout fallback (unaligned rows / huge vocab): K2+K4, then K5
-  float* lp = logp;
-  if (!lp) {
-    PRORL_CUDA(c->logp.ensure(sizeof(float) * (size_t)n_rows));
-    lp = c->logp.as<float>();
-  }
-  PRORL_TRY(launch_score(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, ref_lp,
-                         n_rows, inv_temp, cfg, lp, entropy, c->slab.as<double>(), score_slab_rows(c), false, &used,
-                         S(stream)));
-  PRORL_TRY(launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream)));
-  return launch_grad(c, logits, dtype, row_stride, vocab, rows, targets, lp, old_lp, adv, row_seq, ref_lp, n_rows,
-                     inv_temp, cfg, n_global, grad, grad_stride, dlogp, S(stream));
+  PRORL_TRY(launch_train(c, logits, dtype, row_stride, vocab, rows, targets, old_lp, adv, row_seq, row_turn, ref_lp,
+                         n_rows, inv_temp, cfg, n_global, logp, entropy, dlogp, grad, c->slab.as<double>(), false,
+                         &used, S(stream)));
+  return launch_slab_reduce(c->slab.as<double>(), used, partials_dev, S(stream));
 }
 
 int prorl_lmhead_logprob(prorl_ctx* c, const void* hidden, int64_t h_stride, const void* weight, int64_t w_stride,

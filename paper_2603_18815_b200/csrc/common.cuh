@@ -103,9 +103,7 @@ int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_strid
                 const prorl_loss_cfg* cfg, double n_global,
                 void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st);
 // K7 (train.cu): one-pass logprob/entropy + loss epilogue + dL/dlogits.
-int train_cluster_size(int dtype, int32_t vocab, int64_t row_stride, const void* logits, const void* grad);
 int train_slab_rows(prorl_ctx* ctx);
-int train_max_clusters(int cs);
 int launch_train(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
                  const int32_t* targets, const float* old_lp, const float* adv, const int32_t* row_seq,
                  const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float inv_temp,

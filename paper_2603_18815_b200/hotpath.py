@@ -172,7 +172,7 @@ class Scorer:
                    inv_temp: float = 1.0, cfg: LossConfig | None = None, grad=None, partials=None,
                    want_rows: bool = True, want_dlogp: bool = False, vocab: int | None = None, ref_lp=None,
                    stream=None):
-        """(partials, logp, entropy, grad, dlogp): score_rows + logits_grad in one HBM pass per row."""
+        """(partials, logp, entropy, grad, dlogp): score_rows + logits_grad with one HBM read of each row."""
         n = targets.numel()
         dev = targets.device
         if partials is None:
@@ -189,13 +189,6 @@ class Scorer:
                                      inv_temp, C.byref(c), float(n_global), ptr(logp), ptr(ent), ptr(partials),
                                      ptr(grad), grad.stride(0), ptr(dl), _stream(stream)))
         return partials, logp, ent, grad, dl
-
-    @staticmethod
-    def score_grad_cluster(logits: torch.Tensor, vocab: int | None = None, grad=None) -> int:
-        """CTAs per row the one-pass kernel uses for this layout (0 = two-pass K2+K5 path)."""
-        V = vocab if vocab is not None else logits.shape[1]
-        return N.lib.prorl_score_grad_cluster(_DT[logits.dtype], V, logits.stride(0), ptr(logits),
-                                              ptr(grad if grad is not None else logits))
 
     # ---- K6: fused LM head (tcgen05) ----
     def lmhead_logprob(self, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor,

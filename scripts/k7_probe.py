@@ -43,11 +43,9 @@ def timed(fn):
     return e0.elapsed_time(e1) / a.reps
 
 
-from paper_2603_18815_b200 import _native as N  # noqa: E402
-print("co-resident clusters by size:", {cs: N.lib.prorl_score_grad_capacity(cs) for cs in range(1, 9)})
 ms7 = timed(lambda: sc.score_grad(x, t, old, adv, seq, turn, float(n), grad=gout, want_rows=False))
 ms2 = timed(lambda: sc.score_rows(x, t, old, adv, seq, turn))
 ms5 = timed(lambda: sc.logits_grad(x, t, old, old, adv, seq, float(n), grad=gout))
 bpr = 2 * V * x.element_size() + 30
-print(f"cluster {Scorer.score_grad_cluster(x, grad=gout)}  K7 {ms7:.3f} ms ({n * bpr / ms7 / 1e6:.0f} GB/s)  "
+print(f"V {V}  K7 {ms7:.3f} ms ({n * bpr / ms7 / 1e6:.0f} GB/s)  "
       f"K2+K4 {ms2:.3f} ms  K5 {ms5:.3f} ms  two-pass {ms2 + ms5:.3f} ms  speedup {(ms2 + ms5) / ms7:.2f}")
