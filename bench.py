@@ -176,6 +176,32 @@ def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
             "frac_of_nominal_8000": gbs / 8000.0}
 
 
+def measure_train_whole_step(sc, host, cfg, pool, n_active, reps: int = 3) -> dict:
+    """The whole per-GPU TRAINING step through the C-ABI (prorl_score_host,
+    training mode): H2D, K1, K3, K7 per micro-batch (loss partials + bf16
+    dL/dlogits into a gradient pool), all-reduce, D2H; device time."""
+    import numpy as np
+    import torch
+    gpool = [torch.empty_like(b) for b in pool]  # grad_buffers[j % n_pool]: one per logits buffer
+    for _ in range(2):
+        sc.score_host(host, cfg, pool, fill=False, seed=2603, train=True, grad_pool=gpool)
+    torch.cuda.synchronize()
+    tms = []
+    for _ in range(reps):
+        _, tm = sc.score_host(host, cfg, pool, fill=False, seed=2603, train=True, grad_pool=gpool)
+        tms.append(tm)
+    torch.cuda.synchronize()
+    seg = np.mean(np.array(tms), axis=0)
+    dev_ms = float(seg[1] + seg[2] + seg[3])
+    e2e_ms = float(seg.sum())
+    del gpool
+    torch.cuda.empty_cache()
+    return {"path": "prorl_score_host training mode (K1, K3, K7 per micro-batch: loss + bf16 dL/dlogits, all-reduce)",
+            "ms_per_step_device": dev_ms, "ms_per_step_e2e": e2e_ms, "score_ms": float(seg[2]),
+            "masked_tokens_per_s": n_active / (dev_ms / 1e3), "e2e_masked_tokens_per_s": n_active / (e2e_ms / 1e3),
+            "hbm_gbs_k7": n_active * (2 * (2 if cfg.dtype == "bf16" else 4) * cfg.vocab + 30) / (float(seg[2]) / 1e3) / 1e9}
+
+
 def measure_train_step(sc, pool, c, args, reps: int = 10) -> dict:
     """K7 (one-pass training step: logprob/entropy + loss partials + dL/dlogits
     from ONE read of each logits row, thread-block clusters) on one full logits
@@ -434,6 +460,7 @@ def run_ours(args):
     if args.pool >= 2 and not args.no_backward:
         try:
             train_step = measure_train_step(sc, pool, c, args)
+            train_step["whole_step"] = measure_train_whole_step(sc, host, cfg, pool, shard.n_active)
         except Exception as ex:
             train_step = {"error": repr(ex)}
     lmhead = measure_lmhead(sc, c, args) if not args.no_backward and c["dtype"] == "bf16" else None

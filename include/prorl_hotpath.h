@@ -315,11 +315,23 @@ typedef int (*prorl_logits_fn)(void* user, int64_t row0, int64_t n, const int32_
 typedef int (*prorl_hidden_fn)(void* user, int64_t row0, int64_t n, const int32_t* d_rows,
                                const int32_t* d_seq, const int32_t* d_cu_seqlens,
                                const void** d_hidden, int64_t* h_stride, void* stream);
+/* Training mode (train != 0, logits path only): each micro-batch runs K7 —
+ * loss partials AND dL/dlogits of the token-mean DAPO loss over n_global
+ * active rows (n_global <= 0: this shard's own active-row count; with more
+ * than one rank the caller passes the global count) — written in place into
+ * the micro-batch's logits buffer, or into grad_buffers[j % n_pool] when
+ * given (same row stride). consume_grad (nullable) then receives the
+ * micro-batch's gradient rows, stream-ordered, before the buffer is reused
+ * (the LM-head backward of the trainer); a non-zero return aborts the step. */
+typedef int (*prorl_grad_fn)(void* user, int64_t row0, int64_t n, const void* d_grad, int64_t row_stride,
+                             void* stream);
 typedef struct prorl_logits_pool {
   void* const* buffers; int32_t n_pool; int32_t fill; int64_t row_stride;
   uint64_t seed; float sigma; int32_t pad_;
   prorl_logits_fn provide; void* user;
   prorl_hidden_fn provide_hidden; const void* weight; int64_t w_stride; int32_t d_model; int32_t pad2_;
+  int32_t train; int32_t pad3_; double n_global;
+  void* const* grad_buffers; prorl_grad_fn consume_grad; void* grad_user;
 } prorl_logits_pool;
 
 /* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for

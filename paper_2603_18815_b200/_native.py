@@ -67,7 +67,11 @@ class LogitsPool(C.Structure):
     _fields_ = [("buffers", vp), ("n_pool", C.c_int32), ("fill", C.c_int32), ("row_stride", C.c_int64),
                 ("seed", C.c_uint64), ("sigma", C.c_float), ("pad_", C.c_int32), ("provide", vp), ("user", vp),
                 ("provide_hidden", vp), ("weight", vp), ("w_stride", C.c_int64), ("d_model", C.c_int32),
-                ("pad2_", C.c_int32)]
+                ("pad2_", C.c_int32), ("train", C.c_int32), ("pad3_", C.c_int32), ("n_global", C.c_double),
+                ("grad_buffers", vp), ("consume_grad", vp), ("grad_user", vp)]
+
+# prorl_grad_fn
+GRAD_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp)
 
 # prorl_hidden_fn
 HIDDEN_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int64, C.c_int64, vp, vp, vp, C.POINTER(vp), C.POINTER(C.c_int64), vp)

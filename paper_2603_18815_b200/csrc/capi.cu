@@ -117,7 +117,7 @@ static_assert(sizeof(prorl_packed) == 13 * 8, "prorl_packed layout");
 static_assert(sizeof(prorl_loss_cfg) == 16, "prorl_loss_cfg layout");
 static_assert(sizeof(prorl_score_cfg) == 40, "prorl_score_cfg layout");
 static_assert(sizeof(prorl_host_batch) == 88, "prorl_host_batch layout");
-static_assert(sizeof(prorl_logits_pool) == 88, "prorl_logits_pool layout");
+static_assert(sizeof(prorl_logits_pool) == 128, "prorl_logits_pool layout");
 static_assert(sizeof(prorl_ingest_result) == 112, "prorl_ingest_result layout");
 
 extern "C" {
@@ -423,6 +423,9 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   if (lmhead_mode && (!pool->weight || pool->d_model <= 0))
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: lm-head mode needs weight and d_model");
   if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
+  const bool train_mode = pool->train != 0;
+  if (train_mode && lmhead_mode)
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: training mode needs the logits path (no fused LM head)");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
   if ((hb->n_turns > 0 && !hb->turns) || (hb->n_tokens > 0 && (!hb->ids || !hb->lp)) ||
@@ -527,8 +530,9 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
                         cfg->adv_eps, 0.0, c->adv.as<float>(), c->informative.as<uint8_t>(), partials, st));
   PRORL_CUDA(cudaEventRecord(c->ev[2], st));
 
-  // ---- K2+K4 over logits micro-batches (or K6 + K4 from hidden states) ----
+  // ---- K2+K4 (K7 in training mode) over logits micro-batches, or K6 + K4 from hidden states ----
   const int64_t mb = cfg->microbatch_rows;
+  const double n_global = pool->n_global > 0.0 ? pool->n_global : (double)std::max<int64_t>(A, 1);
   for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
     const int64_t n = std::min(mb, A - row0);
     if (lmhead_mode) {
@@ -569,6 +573,25 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
                                          pk.act_target + row0, pk.act_old_lp + row0, pool->seed, pool->sigma, st));
       }
       buf = b;
+    }
+    if (train_mode) {
+      void* grad = pool->grad_buffers ? pool->grad_buffers[j % std::max(pool->n_pool, 1)] : const_cast<void*>(buf);
+      const int esz = cfg->dtype == PRORL_BF16 ? 2 : 4;
+      if (!grad || reinterpret_cast<uintptr_t>(buf) % esz ||
+          (static_cast<const uint8_t*>(grad) - static_cast<const uint8_t*>(buf)) % 16 != 0)
+        return fail(PRORL_E_SHAPE, "prorl_score_host: gradient buffer must share the logits' 16-byte phase");
+      int used = 0;
+      PRORL_TRY(launch_train(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
+                             pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr,
+                             n, cfg->inv_temperature, &cfg->loss, n_global, nullptr, nullptr, nullptr, grad, slab, true,
+                             &used, st));
+      if (pool->consume_grad) {
+        const int rc = pool->consume_grad(pool->grad_user, row0, n, grad, stride, stream);
+        if (rc != PRORL_OK)
+          return fail(rc, "prorl_score_host: gradient callback failed with status " + std::to_string(rc) +
+                              " at micro-batch " + std::to_string(j));
+      }
+      continue;
     }
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
                            pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr, n,

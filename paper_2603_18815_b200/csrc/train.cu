@@ -89,7 +89,12 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
     if ((k & 255u) == 0) {
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 4000000000ull) __trap();
+      if (t - t0 > 4000000000ull) {
+#ifdef PRORL_K7_DEBUG
+        printf("k_train stuck: block %d warp %d bar %p parity %u\n", blockIdx.x, (int)(threadIdx.x >> 5), bar, parity);
+#endif
+        __trap();
+      }
     }
   }
 }

@@ -251,7 +251,8 @@ class Scorer:
         hb = batch.c()
         dummy = (C.c_void_p * 1)(None)
         lp = N.LogitsPool(C.cast(dummy, C.c_void_p), 0, 0, 0, 0, 0.0, 0, None, None,
-                          C.cast(fn, C.c_void_p), ptr(weight), weight.stride(0), weight.shape[1], 0)
+                          C.cast(fn, C.c_void_p), ptr(weight), weight.stride(0), weight.shape[1], 0,
+                          0, 0, 0.0, None, None, None)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()
@@ -261,11 +262,28 @@ class Scorer:
 
     # ---- whole per-GPU step from host buffers ----
     def score_host(self, batch: "HostBatchArrays", cfg: ScoreConfig, pool: list[torch.Tensor], fill: bool,
-                   seed: int = 0, sigma: float = 2.0, stream=None):
+                   seed: int = 0, sigma: float = 2.0, stream=None, train: bool = False, n_global: float = 0.0,
+                   grad_pool: list[torch.Tensor] | None = None, grad_fn=None):
+        """Whole step through prorl_score_host. train=True runs K7 per micro-batch (loss partials + dL/dlogits,
+        in place or into grad_pool); grad_fn(row0, n, grad_ptr, row_stride) sees each micro-batch's gradient."""
+        if grad_pool is not None and len(grad_pool) != len(pool):
+            raise ValueError("grad_pool needs one buffer per logits buffer (grad_buffers[j % n_pool])")
         hb = batch.c()
         bufs = (C.c_void_p * len(pool))(*[ptr(b) for b in pool])
+        gbufs = (C.c_void_p * len(grad_pool))(*[ptr(b) for b in grad_pool]) if grad_pool else None
+        cb = None
+        if grad_fn is not None:
+            def _cb(user, row0, n, g, stride, strm):
+                try:
+                    grad_fn(row0, n, g, stride)
+                    return 0
+                except Exception:  # noqa: BLE001 — reported as a C status
+                    return -3
+            cb = N.GRAD_FN(_cb)
         lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0,
-                          None, None, None, None, 0, 0, 0)
+                          None, None, None, None, 0, 0, 0, 1 if train else 0, 0, float(n_global),
+                          C.cast(gbufs, C.c_void_p) if gbufs is not None else None,
+                          C.cast(cb, C.c_void_p) if cb is not None else None, None)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()

@@ -186,3 +186,47 @@ def test_score_grad_full_microbatch_properties(scorer, cuda):
     s = x.float().sum(dim=1)
     mx = x.float().abs().amax(dim=1)
     assert torch.isfinite(s).all() and bool((s.abs() <= V * 2.0 ** -8 * mx + 1e-12).all())
+
+
+def test_score_host_train_mode(scorer, cuda):
+    """prorl_score_host in training mode (K7 per micro-batch): partials equal the
+    forward step's, and each micro-batch's gradient equals prorl_score_grad on
+    the same logits with the device-packed rows and GRPO advantages."""
+    from paper_2603_18815_b200 import synth
+    from paper_2603_18815_b200.hotpath import ScoreConfig
+    from tests.test_gpu_parity import device_pack
+    sh = synth.make_shard("c1", seed=5)
+    b = sh.batch
+    V, mb = 32000, 2048
+    cfg = ScoreConfig(vocab=V, dtype="fp32", microbatch_rows=mb)
+    n_mb = -(-sh.n_active // mb)
+    pool = [torch.empty((mb, V), dtype=torch.float32, device=cuda) for _ in range(n_mb)]  # no buffer reuse
+    gpool = [torch.empty_like(p) for p in pool]
+    seen = []
+    fwd, _ = scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7)
+    trn, tm = scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7, train=True, grad_pool=gpool,
+                                grad_fn=lambda r0, n, g, s: seen.append((r0, n, g, s)))
+    torch.cuda.synchronize()
+    assert [(r0, n) for r0, n, _, _ in seen] == [(j * mb, min(mb, sh.n_active - j * mb)) for j in range(n_mb)]
+    assert all(g == gpool[j].data_ptr() and s == V for j, (_, _, g, s) in enumerate(seen))
+    assert trn[N.P_N_ACTIVE] == fwd[N.P_N_ACTIVE] == sh.n_active
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM, N.P_ADV_SUM):
+        assert abs(trn[i] - fwd[i]) <= 2e-5 * abs(fwd[i]) + 1e-6, (i, trn[i], fwd[i])
+    # reference: prorl_score_grad on the same (regenerated) logits
+    pk = device_pack(scorer, b, V, sh.n_active, cuda)
+    adv, _ = scorer.grpo_adv(torch.from_numpy(b.reward).to(cuda), torch.from_numpy(b.usable).to(cuda),
+                             torch.from_numpy(b.group_off).to(cuda))
+    for j in range(n_mb):
+        r0, n = j * mb, min(mb, sh.n_active - j * mb)
+        sl = slice(r0, r0 + n)
+        _, _, _, g_ref, _ = scorer.score_grad(pool[j][:n], pk["act_target"][sl], pk["act_old_lp"][sl], adv,
+                                               pk["act_seq"][sl], pk["act_turn"][sl], float(sh.n_active))
+        torch.cuda.synchronize()
+        assert torch.equal(gpool[j][:n], g_ref[:n])
+    # in place (no grad pool): the logits buffers end up holding the gradient
+    trn2, _ = scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7, train=True)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.from_numpy(trn2), torch.from_numpy(trn))
+    for j in range(n_mb):
+        n = min(mb, sh.n_active - j * mb)
+        assert torch.equal(pool[j][:n], gpool[j][:n])
