@@ -77,6 +77,17 @@ class LogitsSource {
                              void* stream) = 0;
 };
 
+// The LM-head backward: receives dL/dlogits of one micro-batch (active rows
+// [row0, row0 + n), same dtype and row stride as the logits the source
+// returned — the gradient overwrites them in place), stream-ordered, before the
+// source is asked for the next micro-batch.
+class GradSink {
+ public:
+  virtual ~GradSink() = default;
+  virtual void gradient(std::int64_t row0, std::int64_t n, const void* d_grad, std::int64_t row_stride,
+                        void* stream) = 0;
+};
+
 // Deterministic synthetic LM head (include/prorl_synth.h) — bench / tests.
 class SyntheticLogits : public LogitsSource {
  public:
@@ -142,6 +153,16 @@ class DeviceScorer {
   // Same on a raw C-ABI batch view (e.g. from ingest_responses).
   ScoreResult score_view(const prorl_host_batch& batch, LogitsSource& logits, const ScoreConfig& cfg,
                          void* stream = nullptr);
+
+  // Training step: the same partials plus dL/dlogits of the token-mean DAPO
+  // loss over n_global active rows (<= 0: this shard's own count; pass the
+  // global count when several ranks train), one HBM read and one HBM write per
+  // logits row (K7). The gradient is written in place into the buffer the
+  // source returned and handed to `grads` per micro-batch.
+  ScoreResult train_groups(const std::vector<PromptGroup>& groups, LogitsSource& logits, GradSink& grads,
+                           const ScoreConfig& cfg, double n_global = 0.0, void* stream = nullptr);
+  ScoreResult train_view(const prorl_host_batch& batch, LogitsSource& logits, GradSink& grads,
+                         const ScoreConfig& cfg, double n_global = 0.0, void* stream = nullptr);
 
   prorl_ctx* ctx() const { return ctx_; }
 

@@ -187,6 +187,44 @@ int provide_logits(void* user, std::int64_t row0, std::int64_t n, const std::int
 }
 }  // namespace
 
+namespace {
+struct GradTrampoline {
+  GradSink* sink;
+  std::string error;
+  int status = PRORL_OK;
+};
+
+int consume_grad(void* user, std::int64_t row0, std::int64_t n, const void* d_grad, std::int64_t row_stride,
+                 void* stream) {
+  auto* t = static_cast<GradTrampoline*>(user);
+  try {
+    t->sink->gradient(row0, n, d_grad, row_stride, stream);
+    return PRORL_OK;
+  } catch (const Error& e) {
+    t->error = e.code() + ": " + e.what();
+  } catch (const std::exception& e) {
+    t->error = e.what();
+  }
+  t->status = PRORL_E_MALFORMED_REQUEST;
+  return t->status;
+}
+
+prorl_score_cfg to_c(const ScoreConfig& cfg) {
+  prorl_score_cfg c{};
+  c.loss.eps_lo = cfg.eps_lo;
+  c.loss.eps_hi = cfg.eps_hi;
+  c.loss.n_buckets = cfg.max_turn_buckets;
+  c.loss.kl_coef = cfg.kl_coef;
+  c.inv_temperature = cfg.inv_temperature;
+  c.adv_eps = cfg.adv_eps;
+  c.ddof = cfg.ddof;
+  c.vocab = cfg.vocab;
+  c.dtype = (int)cfg.dtype;
+  c.microbatch_rows = cfg.microbatch_rows;
+  return c;
+}
+}  // namespace
+
 ScoreResult DeviceScorer::score_batch(const HostBatch& batch, LogitsSource& logits, const ScoreConfig& cfg,
                                       void* stream) {
   return score_view(batch.view(), logits, cfg, stream);
@@ -210,17 +248,7 @@ IngestedBatch::~IngestedBatch() { prorl_ingest_free(&r_); }
 
 ScoreResult DeviceScorer::score_view(const prorl_host_batch& hb, LogitsSource& logits, const ScoreConfig& cfg,
                                      void* stream) {
-  prorl_score_cfg c{};
-  c.loss.eps_lo = cfg.eps_lo;
-  c.loss.eps_hi = cfg.eps_hi;
-  c.loss.n_buckets = cfg.max_turn_buckets;
-  c.loss.kl_coef = cfg.kl_coef;
-  c.inv_temperature = cfg.inv_temperature;
-  c.adv_eps = cfg.adv_eps;
-  c.ddof = cfg.ddof;
-  c.vocab = cfg.vocab;
-  c.dtype = (int)cfg.dtype;
-  c.microbatch_rows = cfg.microbatch_rows;
+  const prorl_score_cfg c = to_c(cfg);
   Trampoline tr{&logits, {}, PRORL_OK};
   prorl_logits_pool pool{};
   pool.provide = &provide_logits;
@@ -238,6 +266,35 @@ ScoreResult DeviceScorer::score_view(const prorl_host_batch& hb, LogitsSource& l
 ScoreResult DeviceScorer::score_groups(const std::vector<PromptGroup>& groups, LogitsSource& logits,
                                        const ScoreConfig& cfg, void* stream) {
   return score_batch(build_host_batch(groups, cfg), logits, cfg, stream);
+}
+
+ScoreResult DeviceScorer::train_view(const prorl_host_batch& hb, LogitsSource& logits, GradSink& grads,
+                                     const ScoreConfig& cfg, double n_global, void* stream) {
+  const prorl_score_cfg c = to_c(cfg);
+  Trampoline tr{&logits, {}, PRORL_OK};
+  GradTrampoline gt{&grads, {}, PRORL_OK};
+  prorl_logits_pool pool{};
+  pool.provide = &provide_logits;
+  pool.user = &tr;
+  pool.train = 1;
+  pool.n_global = n_global;
+  pool.consume_grad = &consume_grad;
+  pool.grad_user = &gt;
+  double partials[PRORL_N_PARTIALS];
+  float tm[5];
+  const int st = prorl_score_host(ctx_, &hb, &c, &pool, partials, tm, stream);
+  if (st != PRORL_OK && tr.status != PRORL_OK) throw MalformedRequest("logits source failed: " + tr.error);
+  if (st != PRORL_OK && gt.status != PRORL_OK) throw MalformedRequest("gradient sink failed: " + gt.error);
+  throw_status(st);
+  ScoreResult r = finalize(partials, cfg.max_turn_buckets);
+  std::memcpy(r.timings_ms, tm, sizeof tm);
+  return r;
+}
+
+ScoreResult DeviceScorer::train_groups(const std::vector<PromptGroup>& groups, LogitsSource& logits,
+                                       GradSink& grads, const ScoreConfig& cfg, double n_global, void* stream) {
+  const HostBatch b = build_host_batch(groups, cfg);
+  return train_view(b.view(), logits, grads, cfg, n_global, stream);
 }
 
 // ---- wire ingestion ---------------------------------------------------------------

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <string>
 
+#include <cuda_runtime.h>
+
 #include "rollout/trainer/scoring.hpp"
 
 using namespace rollout;
@@ -255,7 +257,48 @@ static int gpu_run() {
   for (std::size_t i = 0; i < hb.group_off.size(); ++i) std::printf("%s%d", i ? "," : "", hb.group_off[i]);
   std::printf("],");
   print_array("partials", r.partials);
-  std::printf(",\"loss\":%.17g,\"n_active\":%lld,\"per_turn\":%zu}\n", r.loss, (long long)r.n_active, r.per_turn.size());
+  std::printf(",\"loss\":%.17g,\"n_active\":%lld,\"per_turn\":%zu,", r.loss, (long long)r.n_active,
+              r.per_turn.size());
+
+  // training step through the façade: gradient per micro-batch handed to a sink
+  struct Sink : GradSink {
+    int V;
+    std::vector<std::pair<long long, long long>> batches;
+    double max_row_sum_rel = 0.0;
+    bool finite = true;
+    long long nonzero_rows = 0;
+    void gradient(std::int64_t row0, std::int64_t n, const void* d_grad, std::int64_t row_stride,
+                  void* stream) override {
+      batches.emplace_back(row0, n);
+      std::vector<std::uint16_t> h((size_t)n * row_stride);
+      cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+      cudaMemcpy(h.data(), d_grad, h.size() * 2, cudaMemcpyDeviceToHost);
+      for (std::int64_t i = 0; i < n; ++i) {
+        double sum = 0.0, mx = 0.0;
+        for (int v = 0; v < V; ++v) {
+          std::uint32_t b = (std::uint32_t)h[(size_t)i * row_stride + v] << 16;
+          float f;
+          std::memcpy(&f, &b, 4);
+          if (!std::isfinite(f)) finite = false;
+          sum += f;
+          mx = std::max(mx, (double)std::fabs(f));
+        }
+        if (mx > 0) {
+          ++nonzero_rows;
+          max_row_sum_rel = std::max(max_row_sum_rel, std::fabs(sum) / mx);
+        }
+      }
+    }
+  } sink;
+  sink.V = V;
+  SyntheticLogits lm2(0, V, cfg.dtype, cfg.microbatch_rows, /*seed=*/4242, 2.0f);
+  const ScoreResult tr = scorer.train_groups(groups, lm2, sink, cfg);
+  print_array("train_partials", tr.partials);
+  std::printf(",\"grad_batches\":[");
+  for (std::size_t i = 0; i < sink.batches.size(); ++i)
+    std::printf("%s[%lld,%lld]", i ? "," : "", sink.batches[i].first, sink.batches[i].second);
+  std::printf("],\"grad_finite\":%d,\"grad_nonzero_rows\":%lld,\"grad_max_row_sum_rel\":%.6g}\n",
+              sink.finite ? 1 : 0, sink.nonzero_rows, sink.max_row_sum_rel);
   return 0;
 }
 

@@ -22,8 +22,9 @@ def binary():
     BIN.parent.mkdir(parents=True, exist_ok=True)
     src = ROOT / "tests" / "cpp" / "test_scoring.cpp"
     if not BIN.exists() or BIN.stat().st_mtime < max(src.stat().st_mtime, B.LIB.stat().st_mtime):
-        cmd = ["g++", "-std=c++17", "-O2", "-Wall", f"-I{ROOT / 'include'}", f"-I{B.json_include()}", str(src),
-               "-o", str(BIN), f"-L{B.PKG}", "-lprorl_hotpath", f"-Wl,-rpath,{B.PKG}"]
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", f"-I{ROOT / 'include'}", f"-I{B.json_include()}",
+               "-I/usr/local/cuda/include", str(src), "-o", str(BIN), f"-L{B.PKG}", "-lprorl_hotpath",
+               f"-Wl,-rpath,{B.PKG}", "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64"]
         subprocess.run(cmd, check=True)
     return BIN
 
@@ -57,6 +58,16 @@ def test_cpp_score_groups_vs_oracle(binary):
     assert got[N.P_N_ACTIVE] == P[N.P_N_ACTIVE]
     assert got[N.P_N_ROLLOUTS] == P[N.P_N_ROLLOUTS]
     assert abs(got[N.P_CLIP_LO] - P[N.P_CLIP_LO]) <= ref["n_border"]
+    # DeviceScorer::train_groups: same partials (K7), one gradient hand-off per
+    # micro-batch, gradient rows finite and summing to ~0 (sum_v (1[v=y] - p_v) = 0)
+    tp = np.array(d["train_partials"])
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM):
+        assert abs(tp[i] - P[i]) <= 1e-5 * Q[i], (i, tp[i], P[i])
+    assert tp[N.P_N_ACTIVE] == P[N.P_N_ACTIVE]
+    n, mb = d["n_active"], 64
+    assert d["grad_batches"] == [[r0, min(mb, n - r0)] for r0 in range(0, n, mb)]
+    assert d["grad_finite"] == 1 and d["grad_nonzero_rows"] > 0
+    assert d["grad_max_row_sum_rel"] <= 4099 * 2.0 ** -8
 
 
 @pytest.mark.gpu
