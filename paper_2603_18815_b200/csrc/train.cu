@@ -40,13 +40,9 @@ namespace {
 
 using namespace rowmath;
 
-constexpr int kUnit = 4096;                  // bytes per warp work unit
-constexpr int kNV = kUnit / 512;             // 16-B vectors per lane per unit
-constexpr int kSplit = 4;                    // units per TMA piece
-constexpr int kPiece = kUnit * kSplit;       // 16 KB per bulk copy
+constexpr int kPiece = 16384;                // bytes per bulk copy (ring slot)
 constexpr int kRing = 12;                    // ring pieces: 192 KB
-constexpr int kWarps = 16;                   // consumer warps (+1 producer warp)
-constexpr int kThreads = (kWarps + 1) * 32;
+constexpr int kMaxWarps = 32;                // consumer warps of any launch configuration
 
 struct TrainArgs {
   const uint8_t* logits;
@@ -99,8 +95,9 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ void consumers_sync() {  // named barrier 1: the consumer warps only
-  asm volatile("bar.sync 1, %0;" ::"r"(kWarps * 32) : "memory");
+template <int W>
+__device__ __forceinline__ void consumers_sync() {  // named barrier 1: the W consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");
 }
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
@@ -179,7 +176,7 @@ struct RowGeo {
   int npc, nsub, head, tail;
 };
 
-template <int ES>
+template <int ES, int kUnit>
 __device__ __forceinline__ RowGeo row_geo(const TrainArgs& p, int64_t i) {
   RowGeo g;
   const int64_t r = p.rows ? (int64_t)p.rows[i] : i;
@@ -208,15 +205,21 @@ __device__ __forceinline__ int64_t edge_index(const RowGeo& g, int l) {
   return -1;
 }
 
-template <typename T, int SUBV>
-__global__ void __launch_bounds__(kThreads, 1) k_train(const TrainArgs p) {
+// W consumer warps + 1 producer warp; UNIT-byte warp work units (kPiece / UNIT per piece).
+template <typename T, int SUBV, int W, int UNIT>
+__global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
   constexpr int ES = Elem<T>::kSize;
+  constexpr int kWarps = W;
+  constexpr int kUnit = UNIT;
+  constexpr int kNV = kUnit / 512;         // 16-B vectors per lane per unit
+  constexpr int kSplit = kPiece / kUnit;   // units per piece
+  static_assert(kNV % SUBV == 0 && kPiece % kUnit == 0 && W <= kMaxWarps, "launch configuration");
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kRing * kPiece);
   uint64_t* empty = full + kRing;
   float4* wpart = reinterpret_cast<float4*>(empty + kRing);   // [2][kWarps] warp partials (row parity)
-  double* gsum = reinterpret_cast<double*>(wpart + 2 * kWarps);  // [kNG]
+  double* gsum = reinterpret_cast<double*>(wpart + 2 * kMaxWarps);  // [kNG]
   double* bk = gsum + kNG;                                      // [kBucketDoubles]
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train(const TrainArgs p) {
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t pc = 0;
       for (int64_t i = blockIdx.x; i < p.n_rows; i += gridDim.x) {
-        const RowGeo g = row_geo<ES>(p, i);
+        const RowGeo g = row_geo<ES, kUnit>(p, i);
         for (int pass = 0; pass < 2; ++pass) {
           for (int k = 0; k < g.npc; ++k, ++pc) {
             const int s = (int)(pc % kRing);
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train(const TrainArgs p) {
   uint32_t pcb = 0;  // ring piece counter at the start of the row
   uint32_t j = 0;    // rows done by this CTA
   for (int64_t i = blockIdx.x; i < p.n_rows; i += gridDim.x, ++j) {
-    const RowGeo g = row_geo<ES>(p, i);
+    const RowGeo g = row_geo<ES, kUnit>(p, i);
     const int32_t y = p.targets[i];
     float xy = 0.f, old = 0.f, A = 0.f, ref = 0.f;
     if (lane == 0) {
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train(const TrainArgs p) {
     }
     float4* wp = wpart + (j & 1) * kWarps;
     if (lane == 0) wp[warp] = make_float4(top.Mc, top.Mx, Sr, Tr);
-    consumers_sync();
+    consumers_sync<W>();
     // every warp merges the 16 partials with the same tree -> identical results
     float4 G = lane < kWarps ? wp[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -462,22 +465,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_train(const TrainArgs p) {
 }
 
 constexpr size_t train_smem_bytes() {
-  return (size_t)kRing * kPiece + (size_t)(2 * kRing) * 8 + (size_t)(2 * kWarps) * 16 +
+  return (size_t)kRing * kPiece + (size_t)(2 * kRing) * 8 + (size_t)(2 * kMaxWarps) * 16 +
          (size_t)(kNG + kBucketDoubles) * 8;
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 static_assert(((size_t)kRing * kPiece + (size_t)(2 * kRing) * 8) % 16 == 0, "float4 partials alignment");
 
-template <typename T>
-int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
-  auto kern = k_train<T, sizeof(T) == 2 ? 8 : 4>;
+// Launch configurations (consumer warps x unit bytes); PRORL_K7_CONFIG selects.
+constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w20u4096", "w24u2048", "w12u4096", "w24u4096"};
+constexpr int kK7Default = 0;
+
+int k7_config() {
+  static int idx = [] {
+    const char* e = std::getenv("PRORL_K7_CONFIG");
+    if (e)
+      for (int i = 0; i < (int)(sizeof(kK7Configs) / sizeof(kK7Configs[0])); ++i)
+        if (std::strcmp(e, kK7Configs[i]) == 0) return i;
+    return kK7Default;
+  }();
+  return idx;
+}
+
+template <typename T, int W, int UNIT>
+int run_train_cfg(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
+  constexpr int SUBV_BF16 = UNIT / 512 >= 8 ? 8 : UNIT / 512;
+  auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT>;
   constexpr size_t smem = train_smem_bytes();
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)std::min<int64_t>((int64_t)n_sm, a.n_rows);
   *rows_used = grid;
-  kern<<<grid, kThreads, smem, st>>>(a);
+  kern<<<grid, (W + 1) * 32, smem, st>>>(a);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
+}
+
+template <typename T>
+int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
+  switch (k7_config()) {
+    case 1: return run_train_cfg<T, 16, 2048>(a, n_sm, rows_used, st);
+    case 2: return run_train_cfg<T, 20, 4096>(a, n_sm, rows_used, st);
+    case 3: return run_train_cfg<T, 24, 2048>(a, n_sm, rows_used, st);
+    case 4: return run_train_cfg<T, 12, 4096>(a, n_sm, rows_used, st);
+    case 5: return run_train_cfg<T, 24, 4096>(a, n_sm, rows_used, st);
+    default: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
+  }
 }
 
 }  // namespace
