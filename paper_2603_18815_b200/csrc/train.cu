@@ -7,22 +7,27 @@
 // K2 then K5 move 2V + 4V bytes of HBM per bf16 row: the backward re-reads the
 // row from HBM after the forward has produced its lse. K7 moves 4V.
 //
-//   * One CTA per SM, persistent over rows; a CTA owns ONE row at a time, so
-//     the rows in flight (148 x 2V = 45 MB at V = 151 936 bf16) fit in the
-//     126 MB L2 between the two passes over each row.
-//   * Pass A (statistics) streams the row from HBM into a shared-memory ring
-//     of 16 KB pieces (1-D TMA bulk copies issued by a producer warp, L2
-//     evict_last); 16 consumer warps take 4 KB units round robin and run K2's
-//     online base-2 logsumexp (warp-uniform running max, top element kept out
-//     of the sums). The 16 warp partials meet in shared memory after one named
-//     barrier; every warp merges them with the same fixed tree, so all hold
-//     bit-identical lse / logp / loss terms.
-//   * Pass B (gradient) streams the same row again — from L2 (evict_first) —
-//     and writes grad = s (1[v = y] - p_v) as 16-B streaming stores. The
-//     producer runs ahead across passes and rows, so the next pieces are
-//     already landing while a pass finishes.
-//   * Warp 0 lane 0 keeps the loss epilogue (fp64 partials + per-turn buckets,
-//     fixed order) and writes one slab row per CTA (deterministic).
+//   * One CTA per SM, persistent over rows. The CTA's consumer warps form G row
+//     groups (G = 2 for rows <= 160 KB, else 1); a group owns ONE row at a
+//     time, so the rows in flight (148 x G x 2V bytes: 45 MB at V = 151 936
+//     bf16) fit in the 126 MB L2 between the two passes over each row, and one
+//     group's barrier and pipeline bubbles overlap the other group's work.
+//   * Pass A (statistics): the group's producer warp streams the row from HBM
+//     into the group's shared-memory ring of 16 KB pieces (1-D TMA bulk
+//     copies, L2 evict_last). Piece P goes to a fixed set of kSplit warps, one
+//     4 KB unit each, so every warp sees every round of its ring slots in
+//     order (a parity wait never aliases a round two phases back; pieces can
+//     complete out of order). Warps run K2's online base-2 logsumexp
+//     (warp-uniform running max, top element kept out of the sums); the warp
+//     partials meet in shared memory after one named barrier and every warp
+//     merges them with the same fixed tree, so all hold bit-identical lse /
+//     logp / loss terms.
+//   * Pass B (gradient): the producer streams the same row again — from L2
+//     (evict_first) — and the warps write grad = s (1[v = y] - p_v) as 16-B
+//     streaming stores. The producer runs ahead across passes and rows.
+//   * One lane per group keeps the loss epilogue (fp64 partials + per-turn
+//     buckets, fixed order); the groups' sums merge in fixed order into one
+//     slab row per CTA (deterministic).
 //
 // Any row layout K2/K5 accept works: the 16-B aligned interior of each row goes
 // through TMA, the < 16-B head/tail elements are handled by warp 0 directly;
@@ -95,10 +100,8 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
   }
 }
 
-template <int W>
-__device__ __forceinline__ void consumers_sync() {  // named barrier 1: the W consumer warps only
-  asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory");
-}
+// named barrier `id` over `n` threads (the producer warps never join one)
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t pol;
@@ -205,45 +208,64 @@ __device__ __forceinline__ int64_t edge_index(const RowGeo& g, int l) {
   return -1;
 }
 
-// W consumer warps + 1 producer warp; UNIT-byte warp work units (kPiece / UNIT per piece).
-template <typename T, int SUBV, int W, int UNIT>
-__global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
+// W consumer warps + G producer warps; UNIT-byte warp work units (kPiece / UNIT
+// per piece). G row groups: group g (W / G consumer warps, kRing / G ring
+// pieces, producer warp W + g) takes every G-th row of the CTA, so one group's
+// barrier and pipeline bubbles overlap the other's work (G = 1: one group).
+template <typename T, int SUBV, int W, int UNIT, int G>
+__global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
   constexpr int ES = Elem<T>::kSize;
-  constexpr int kWarps = W;
+  constexpr int kWarps = W / G;      // consumer warps per group
+  constexpr int kRG = kRing / G;     // ring pieces per group
   constexpr int kUnit = UNIT;
   constexpr int kNV = kUnit / 512;         // 16-B vectors per lane per unit
   constexpr int kSplit = kPiece / kUnit;   // units per piece
-  static_assert(kNV % SUBV == 0 && kPiece % kUnit == 0 && W <= kMaxWarps, "launch configuration");
+  // Piece P of a group's ring stream is consumed by the kSplit warps
+  // kSplit * (P mod kPG) + (0 .. kSplit-1) (one unit each, the last piece of a
+  // pass padded with empty units). kRG is a multiple of kPG, so each ring slot
+  // always has the same kSplit consumers and every consumer observes every
+  // round of its slots in order: a parity wait can never alias a round two
+  // phases behind (pieces may complete out of order).
+  constexpr int kPG = kWarps / kSplit;
+  static_assert(kNV % SUBV == 0 && kPiece % kUnit == 0 && W <= kMaxWarps && W % G == 0 && kRing % G == 0 &&
+                    kWarps % kSplit == 0 && kRG % kPG == 0,
+                "launch configuration");
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kRing * kPiece);
-  uint64_t* empty = full + kRing;
-  float4* wpart = reinterpret_cast<float4*>(empty + kRing);   // [2][kWarps] warp partials (row parity)
-  double* gsum = reinterpret_cast<double*>(wpart + 2 * kMaxWarps);  // [kNG]
-  double* bk = gsum + kNG;                                      // [kBucketDoubles]
+  uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + (size_t)kRing * kPiece);
+  uint64_t* empty_all = full_all + kRing;
+  float4* wpart_all = reinterpret_cast<float4*>(empty_all + kRing);  // [G][2][kWarps] warp partials (row parity)
+  double* gsum_all = reinterpret_cast<double*>(wpart_all + 2 * kMaxWarps);  // [G][kNG + kBucketDoubles]
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp < W ? warp / kWarps : warp - W;  // row group (consumers) / fed group (producers)
+  const int wq = warp < W ? warp % kWarps : 0;          // warp index inside its group
+  uint8_t* ring = smem + (size_t)grp * kRG * kPiece;
+  uint64_t* full = full_all + grp * kRG;
+  uint64_t* empty = empty_all + grp * kRG;
+  float4* wpart = wpart_all + grp * 2 * kWarps;
+  double* gsum = gsum_all + grp * (kNG + kBucketDoubles);  // [kNG]
+  double* bk = gsum + kNG;                                 // [kBucketDoubles]
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kSplit);
+      mbar_init(&full_all[s], 1);
+      mbar_init(&empty_all[s], kSplit);
     }
     fence_mbar_init();
   }
-  for (int t = threadIdx.x; t < kNG + kBucketDoubles; t += blockDim.x) gsum[t] = 0.0;
+  for (int t = threadIdx.x; t < G * (kNG + kBucketDoubles); t += blockDim.x) gsum_all[t] = 0.0;
   __syncthreads();
 
-  if (warp == kWarps) {
+  if (warp >= W) {
     // ===== producer: pass A (HBM, keep in L2) then pass B (L2) of each row =====
-    if (lane == 0) {
+    if (lane == 0 && grp < G) {
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t pc = 0;
-      for (int64_t i = blockIdx.x; i < p.n_rows; i += gridDim.x) {
+      for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x) {
         const RowGeo g = row_geo<ES, kUnit>(p, i);
         for (int pass = 0; pass < 2; ++pass) {
           for (int k = 0; k < g.npc; ++k, ++pc) {
-            const int s = (int)(pc % kRing);
-            mbar_wait_t(&empty[s], ((pc / kRing) & 1) ^ 1);
+            const int s = (int)(pc % kRG);
+            mbar_wait_t(&empty[s], ((pc / kRG) & 1) ^ 1);
             const uint32_t bytes = min((uint32_t)kPiece, g.nb - (uint32_t)k * kPiece);
             mbar_arrive_expect_tx(&full[s], bytes);
             tma_load_1d(ring + (size_t)s * kPiece, reinterpret_cast<const void*>(g.a + (uintptr_t)k * kPiece), bytes,
@@ -262,7 +284,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
   const uint4 fill = make_uint4(Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord);
   uint32_t pcb = 0;  // ring piece counter at the start of the row
   uint32_t j = 0;    // rows done by this CTA
-  for (int64_t i = blockIdx.x; i < p.n_rows; i += gridDim.x, ++j) {
+  for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x, ++j) {
     const RowGeo g = row_geo<ES, kUnit>(p, i);
     const int32_t y = p.targets[i];
     float xy = 0.f, old = 0.f, A = 0.f, ref = 0.f;
@@ -277,19 +299,25 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
     old = __shfl_sync(kFull, old, 0);
     A = __shfl_sync(kFull, A, 0);
     ref = __shfl_sync(kFull, ref, 0);
-    // units of this row start at warp (j * nsub) mod 16, so the extra units of
-    // uneven rows rotate over the warps
-    const int u0 = (int)((((uint32_t)warp + kWarps) - (j * (uint32_t)g.nsub) % kWarps) % kWarps);
+    const int kk = wq % kSplit;  // this warp's unit inside its pieces
+    // first piece (offset from pc0) of a pass that this warp consumes
+    auto first_piece = [&](uint32_t pc0) { return (int)(((uint32_t)(wq / kSplit) + kPG - pc0 % kPG) % kPG); };
 
     // ---- pass A: statistics ----
     Top top{-INFINITY, 0.f};
     float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    for (int u = u0; u < g.nsub; u += kWarps) {
-      const uint32_t pc = pcb + (uint32_t)(u / kSplit);
-      const int s = (int)(pc % kRing);
-      mbar_wait_t(&full[s], (pc / kRing) & 1);
-      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)(u % kSplit) * kUnit);
+    for (int k = first_piece(pcb); k < g.npc; k += kPG) {
+      const uint32_t pc = pcb + (uint32_t)k;
+      const int u = k * kSplit + kk;
+      const int s = (int)(pc % kRG);
+      mbar_wait_t(&full[s], (pc / kRG) & 1);
+      if (u >= g.nsub) {  // padding unit of the pass's last piece
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+        continue;
+      }
+      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
       const uint32_t nvv = min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) >> 4;
       uint4 v[kNV];
       if (nvv == (uint32_t)(kUnit / 16)) {
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[s], u == g.nsub - 1 ? (uint32_t)(kSplit - u % kSplit) : 1u);
+      if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
 #pragma unroll
       for (int g0 = 0; g0 < kNV; g0 += SUBV) {
         uint4 w[SUBV];
@@ -317,7 +345,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
         Elem<T>::template accumulate<SUBV>(w, c2, make_float2(-top.Mc, -top.Mc), S, Tt);
       }
     }
-    if (warp == 0 && g.head + g.tail > 0) {
+    if (wq == 0 && g.head + g.tail > 0) {
       const int64_t idx = edge_index<ES>(g, lane);
       scalar_step(idx >= 0 ? Elem<T>::load(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, S, Tt, lane);
     }
@@ -328,14 +356,15 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
       // share straight from global memory (rare)
       top = Top{-INFINITY, 0.f};
       S[0] = S[1] = Tt[0] = Tt[1] = make_float2(0.f, 0.f);
-      for (int u = u0; u < g.nsub; u += kWarps) {
+      for (int k = first_piece(pcb); k * kSplit + kk < g.nsub; k += kPG) {
+        const int u = k * kSplit + kk;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(g.a + (uintptr_t)u * kUnit);
         const int ne = (int)(min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) / ES);
         for (int b = 0; b < ne; b += 32)
           scalar_step(b + lane < ne ? load_clamped<T>(src, b + lane) : __uint_as_float(0xf0000000u), c, top, S, Tt,
                       lane);
       }
-      if (warp == 0 && g.head + g.tail > 0) {
+      if (wq == 0 && g.head + g.tail > 0) {
         const int64_t idx = edge_index<ES>(g, lane);
         scalar_step(idx >= 0 ? load_clamped<T>(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, S, Tt, lane);
       }
@@ -343,31 +372,31 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
       Tr = warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y));
     }
     float4* wp = wpart + (j & 1) * kWarps;
-    if (lane == 0) wp[warp] = make_float4(top.Mc, top.Mx, Sr, Tr);
-    consumers_sync<W>();
+    if (lane == 0) wp[wq] = make_float4(top.Mc, top.Mx, Sr, Tr);
+    named_sync(1 + grp, kWarps * 32);
     // every warp merges the 16 partials with the same tree -> identical results
-    float4 G = lane < kWarps ? wp[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+    float4 Gp = lane < kWarps ? wp[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int o = 1; o < kWarps; o <<= 1) {
       float4 Q;
-      Q.x = __shfl_down_sync(kFull, G.x, o);
-      Q.y = __shfl_down_sync(kFull, G.y, o);
-      Q.z = __shfl_down_sync(kFull, G.z, o);
-      Q.w = __shfl_down_sync(kFull, G.w, o);
-      const float4 M = merge_partial(G, Q, c);
-      if ((lane & (2 * o - 1)) == 0) G = M;
+      Q.x = __shfl_down_sync(kFull, Gp.x, o);
+      Q.y = __shfl_down_sync(kFull, Gp.y, o);
+      Q.z = __shfl_down_sync(kFull, Gp.z, o);
+      Q.w = __shfl_down_sync(kFull, Gp.w, o);
+      const float4 M = merge_partial(Gp, Q, c);
+      if ((lane & (2 * o - 1)) == 0) Gp = M;
     }
-    G.x = __shfl_sync(kFull, G.x, 0);
-    G.y = __shfl_sync(kFull, G.y, 0);
-    G.z = __shfl_sync(kFull, G.z, 0);
-    G.w = __shfl_sync(kFull, G.w, 0);
+    Gp.x = __shfl_sync(kFull, Gp.x, 0);
+    Gp.y = __shfl_sync(kFull, Gp.y, 0);
+    Gp.z = __shfl_sync(kFull, Gp.z, 0);
+    Gp.w = __shfl_sync(kFull, Gp.w, 0);
 
     // ---- row results ----
-    const float rr = fmaf(G.y, c, -G.x);
+    const float rr = fmaf(Gp.y, c, -Gp.x);
     const float ir = ex2_approx(-rr);
-    const float qq = G.z * ir;
+    const float qq = Gp.z * ir;
     const float l1q = log1pf(qq);
-    const float logp = (fmaf(xy, c, -G.x) - rr) * kLn2 - l1q;
+    const float logp = (fmaf(xy, c, -Gp.x) - rr) * kLn2 - l1q;
     const float ratio = expf(logp - old);
     const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
     float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
@@ -375,8 +404,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
     const float sg = -dl * p.inv_temp;  // grad_v = sg p_v (v != y), grad_y = sg expm1(logp) = -sg (1 - p_y)
     const float l2 = fmaf(xy, c, -logp * kLog2e);
     const float gy = sg * expm1f(logp);
-    if (warp == 0 && lane == 0) {
-      const float ent = l1q + kLn2 * (fmaf(rr, qq, -G.w * ir) / (1.f + qq));
+    if (wq == 0 && lane == 0) {
+      const float ent = l1q + kLn2 * (fmaf(rr, qq, -Gp.w * ir) / (1.f + qq));
       if (p.logp) p.logp[i] = logp;
       if (p.entropy) p.entropy[i] = ent;
       if (p.dlogp) p.dlogp[i] = dl;
@@ -408,11 +437,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
     const int32_t yvec = y_in ? (int32_t)((yb - g.a) >> 4) : -1;
     const int ye = (int)((yb & 15) / ES);
     const uint32_t pcB = pcb + (uint32_t)g.npc;
-    for (int u = u0; u < g.nsub; u += kWarps) {
-      const uint32_t pc = pcB + (uint32_t)(u / kSplit);
-      const int s = (int)(pc % kRing);
-      mbar_wait_t(&full[s], (pc / kRing) & 1);
-      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)(u % kSplit) * kUnit);
+    for (int k = first_piece(pcB); k < g.npc; k += kPG) {
+      const uint32_t pc = pcB + (uint32_t)k;
+      const int u = k * kSplit + kk;
+      const int s = (int)(pc % kRG);
+      mbar_wait_t(&full[s], (pc / kRG) & 1);
+      if (u >= g.nsub) {  // padding unit of the pass's last piece
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+        continue;
+      }
+      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
       const uint32_t nvv = min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) >> 4;
       const int32_t tq = y_in ? yvec - u * (kUnit / 16) : -1;  // target vector inside this unit
       uint4* dst = reinterpret_cast<uint4*>(g.a + (uintptr_t)u * kUnit + (uintptr_t)p.goff);
@@ -423,7 +458,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
         v[jj] = qv < nvv ? sv[qv] : make_uint4(0, 0, 0, 0);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[s], u == g.nsub - 1 ? (uint32_t)(kSplit - u % kSplit) : 1u);
+      if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
 #pragma unroll
       for (int jj = 0; jj < kNV; ++jj) {
         const uint32_t qv = lane + 32 * jj;
@@ -437,7 +472,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
         }
       }
     }
-    if (warp == 0 && g.head + g.tail > 0) {
+    if (wq == 0 && g.head + g.tail > 0) {
       const int64_t idx = edge_index<ES>(g, lane);
       if (idx >= 0) {
         const float x = Elem<T>::load(g.rp, idx);
@@ -451,13 +486,16 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
     pcb += 2u * (uint32_t)g.npc;
   }
 
-  // ---- slab row of this CTA ----
+  // ---- slab row of this CTA: the groups' sums in fixed order ----
+  named_sync(1 + G, W * 32);
   if (warp == 0) {
-    __syncwarp();
     for (int t = lane; t < PRORL_N_PARTIALS; t += 32) {
       double v = 0.0;
-      if (t < kNG) v = gsum[t];
-      else if (t >= PRORL_N_GLOBAL) v = bk[t - PRORL_N_GLOBAL];
+      for (int q = 0; q < G; ++q) {
+        const double* gs = gsum_all + q * (kNG + kBucketDoubles);
+        if (t < kNG) v += gs[t];
+        else if (t >= PRORL_N_GLOBAL) v += gs[kNG + t - PRORL_N_GLOBAL];
+      }
       double* d = p.slab + (size_t)blockIdx.x * PRORL_N_PARTIALS + t;
       *d = p.accumulate ? *d + v : v;
     }
@@ -466,47 +504,55 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k_train(const TrainArgs p) {
 
 constexpr size_t train_smem_bytes() {
   return (size_t)kRing * kPiece + (size_t)(2 * kRing) * 8 + (size_t)(2 * kMaxWarps) * 16 +
-         (size_t)(kNG + kBucketDoubles) * 8;
+         (size_t)2 * (kNG + kBucketDoubles) * 8;
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 static_assert(((size_t)kRing * kPiece + (size_t)(2 * kRing) * 8) % 16 == 0, "float4 partials alignment");
 
 // Launch configurations (consumer warps x unit bytes); PRORL_K7_CONFIG selects.
-constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w20u4096", "w24u2048", "w12u4096", "w24u4096"};
-constexpr int kK7Default = 0;
+constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w24u2048", "w12u4096", "w24u4096", "w16u4096g2",
+                                     "w16u2048g2", "w8u4096"};
+constexpr int kK7Default = 0, kK7TwoGroups = 5;
 
-int k7_config() {
-  static int idx = [] {
+// Default: two row groups per CTA when two rows per SM still fit the L2
+// comfortably (row <= 160 KB: 296 rows in flight <= 48 MB) — measured 1.2-1.3x
+// at V = 32 000 / 65 536 — else one group (2x the rows in flight costs L2 hits:
+// -15 % at V = 151 936 bf16).
+int k7_config(int64_t row_bytes) {
+  static int forced = [] {
     const char* e = std::getenv("PRORL_K7_CONFIG");
     if (e)
       for (int i = 0; i < (int)(sizeof(kK7Configs) / sizeof(kK7Configs[0])); ++i)
         if (std::strcmp(e, kK7Configs[i]) == 0) return i;
-    return kK7Default;
+    return -1;
   }();
-  return idx;
+  if (forced >= 0) return forced;
+  return row_bytes <= 160 * 1024 ? kK7TwoGroups : kK7Default;
 }
 
-template <typename T, int W, int UNIT>
+template <typename T, int W, int UNIT, int G = 1>
 int run_train_cfg(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
   constexpr int SUBV_BF16 = UNIT / 512 >= 8 ? 8 : UNIT / 512;
-  auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT>;
+  auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT, G>;
   constexpr size_t smem = train_smem_bytes();
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)std::min<int64_t>((int64_t)n_sm, a.n_rows);
   *rows_used = grid;
-  kern<<<grid, (W + 1) * 32, smem, st>>>(a);
+  kern<<<grid, (W + G) * 32, smem, st>>>(a);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
 }
 
 template <typename T>
 int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
-  switch (k7_config()) {
+  switch (k7_config((int64_t)a.vocab * (int64_t)sizeof(T))) {
     case 1: return run_train_cfg<T, 16, 2048>(a, n_sm, rows_used, st);
-    case 2: return run_train_cfg<T, 20, 4096>(a, n_sm, rows_used, st);
-    case 3: return run_train_cfg<T, 24, 2048>(a, n_sm, rows_used, st);
-    case 4: return run_train_cfg<T, 12, 4096>(a, n_sm, rows_used, st);
-    case 5: return run_train_cfg<T, 24, 4096>(a, n_sm, rows_used, st);
+    case 2: return run_train_cfg<T, 24, 2048>(a, n_sm, rows_used, st);
+    case 3: return run_train_cfg<T, 12, 4096>(a, n_sm, rows_used, st);
+    case 4: return run_train_cfg<T, 24, 4096>(a, n_sm, rows_used, st);
+    case 5: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, rows_used, st);
+    case 6: return run_train_cfg<T, 16, 2048, 2>(a, n_sm, rows_used, st);
+    case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, rows_used, st);
     default: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
   }
 }
