@@ -267,6 +267,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
             const int s = (int)(pc % kRG);
             mbar_wait_t(&empty[s], ((pc / kRG) & 1) ^ 1);
             const uint32_t bytes = min((uint32_t)kPiece, g.nb - (uint32_t)k * kPiece);
+            fence_proxy_async_smem();  // the consumers' generic reads of this slot before the async-proxy refill
             mbar_arrive_expect_tx(&full[s], bytes);
             tma_load_1d(ring + (size_t)s * kPiece, reinterpret_cast<const void*>(g.a + (uintptr_t)k * kPiece), bytes,
                         &full[s], pass == 0 ? pol_a : pol_b);

@@ -31,6 +31,16 @@ turn = torch.randint(0, 70, (n,), dtype=torch.int16, device=dev)
 s.clipped_loss(lp, ent, old, adv, seq, turn, cfg=LossConfig(kl_coef=1e-4), ref_lp=lp + 0.1)
 s.score_rows(x, t, old, adv, seq, turn, rows=rows, vocab=V)
 s.logits_grad(x, t, lp, old, adv, seq, float(n), rows=rows, vocab=V)
+# K7 one-pass training step: odd vocab / padded stride / row indirection / in place (two row groups),
+# and a large-row bf16 case (one row group, rows longer than the shared-memory ring)
+s.score_grad(x, t, old, adv, seq, turn, float(n), rows=rows, vocab=V, grad=x, want_dlogp=True)
+xl = torch.empty((24, 151936), dtype=torch.bfloat16, device=dev)
+tl = torch.randint(0, 151936, (24,), dtype=torch.int32, device=dev)
+s.gen_logits(xl, 24, 0, tl, old[:24])
+s.score_grad(xl, tl, old[:24], adv, seq[:24], turn[:24], 24.0, cfg=LossConfig(kl_coef=1e-4), ref_lp=old[:24] + 0.1)
+# K7 inside the whole step (training mode, gradient pool)
+gpool = [torch.empty_like(pool[0])]
+s.score_host(b.pinned(), cfg, pool, fill=True, seed=3, train=True, grad_pool=gpool)
 H = torch.randn(200, 256, device=dev).to(torch.bfloat16)
 W = (torch.randn(4099, 256, device=dev) * 0.1).to(torch.bfloat16)
 s.lmhead_logprob(H, W, torch.randint(0, 4099, (200,), dtype=torch.int32, device=dev))
