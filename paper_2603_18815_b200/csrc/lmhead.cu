@@ -21,6 +21,8 @@
 //               out of the sums (as K2), target-logit capture; the two TMEM
 //               accumulators let MMA of tile n+1 overlap the epilogue of n.
 // Output: logp / entropy per row, identical definitions to K2 (App. B.2).
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -67,9 +69,18 @@ __device__ __forceinline__ Unit unit_of(const LmParams& p, int64_t u) {
 }
 
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
-  // bounded spin: a protocol bug traps instead of hanging the GPU
-  for (uint64_t it = 0; !mbar_try_wait(bar, parity); ++it)
-    if (it > (1ull << 31)) __trap();
+  // bounded wait: a protocol bug traps after ~4 s instead of hanging the GPU
+  if (mbar_try_wait(bar, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t k = 1;; ++k) {
+    if (mbar_try_wait(bar, parity)) return;
+    if ((k & 255u) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 4000000000ull) __trap();
+    }
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -126,6 +137,83 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Online logsumexp state of one row (one epilogue thread) over a vocab chunk.
+// Per row: ~V terms. Each 32-column group is summed in 4 chains, then added
+// to the running (S, T) with Kahan compensation (cS, cT), so the fp32 error
+// stays at a few ulps over 150K+ terms; the element that set the running max
+// is kept out of the sums (re-added analytically by the merge).
+struct RowAcc {
+  float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, cS = 0.f, cT = 0.f, xy = 0.f;
+  bool has_y = false;
+};
+
+// Consume one accumulator tile row: 256 fp32 logits at TMEM address `base`
+// (this thread's lane), vocab columns [col0, col0 + ncols).
+__device__ __forceinline__ void epi_tile(uint32_t base, int col0, int ncols, int32_t tgt, float c, RowAcc& a) {
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    float v[32];
+    tmem_ld32(base + (uint32_t)c0, v);
+    if (c0 >= ncols) continue;
+    const int lim = min(32, ncols - c0);
+    const int ty = tgt - col0 - c0;
+    if (ty >= 0 && ty < lim) a.has_y = true;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a.xy = (j == ty) ? v[j] : a.xy;
+    float lm = v[0];
+#pragma unroll
+    for (int j = 1; j < 32; ++j) lm = j < lim ? fmaxf(lm, v[j]) : lm;
+    int excl = -1;
+    if (lm * c > a.Mc) {  // new top element: fold the old one in, rescale, exclude the new one
+#pragma unroll
+      for (int j = 31; j >= 0; --j) excl = (j < lim && v[j] == lm) ? j : excl;
+      const float nMc = lm * c;
+      if (a.Mc != -INFINITY) {
+        const float sc = ex2_approx(a.Mc - nMc), dl = nMc - a.Mc;
+        a.T = sc * fmaf(-dl, a.S, a.T);
+        a.cT = sc * fmaf(-dl, a.cS, a.cT);
+        a.S *= sc;
+        a.cS *= sc;
+        const float d = fmaf(a.Mx, c, -nMc), e = ex2_approx(d);
+        float y = e - a.cS, t = a.S + y;
+        a.cS = (t - a.S) - y;
+        a.S = t;
+        y = d * e - a.cT;
+        t = a.T + y;
+        a.cT = (t - a.T) - y;
+        a.T = t;
+      }
+      a.Mc = nMc;
+      a.Mx = lm;
+    }
+    float gs[4] = {0.f, 0.f, 0.f, 0.f}, gt[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < lim && j != excl) {
+        const float d = fmaf(v[j], c, -a.Mc), e = ex2_approx(d);
+        gs[j & 3] += e;
+        gt[j & 3] = fmaf(d, e, gt[j & 3]);
+      }
+    }
+    float y = ((gs[0] + gs[1]) + (gs[2] + gs[3])) - a.cS, t = a.S + y;
+    a.cS = (t - a.S) - y;
+    a.S = t;
+    y = ((gt[0] + gt[1]) + (gt[2] + gt[3])) - a.cT;
+    t = a.T + y;
+    a.cT = (t - a.T) - y;
+    a.T = t;
+  }
+}
+
+__device__ __forceinline__ void store_partial(const LmParams& p, int64_t grow, int32_t chunk, const RowAcc& a) {
+  float* o = p.part + ((size_t)grow * p.n_chunks + chunk) * 6;
+  o[0] = a.Mc;
+  o[1] = a.Mx;
+  o[2] = a.S;
+  o[3] = a.T;
+  o[4] = a.xy;
+  o[5] = a.has_y ? 1.f : 0.f;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -225,82 +313,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Unit w = unit_of(p, u);
     const int64_t grow = (int64_t)w.m * BM + row;
     const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
-    bool has_y = false;
-    // Per row: ~V terms. Each 32-column group is summed in 4 chains, then added
-    // to the running (S, T) with Kahan compensation (cS, cT), so the fp32
-    // error stays at a few ulps over 150K+ terms.
-    float Mc = -INFINITY, Mx = 0.f, S = 0.f, T = 0.f, cS = 0.f, cT = 0.f, xy = 0.f;
+    RowAcc a;
     for (int n = w.t0; n < w.t1; ++n, ++tile) {
       const int acc = tile & 1;
       mbar_wait_bounded(&tfull[acc], (tile >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      const int col0 = n * BN;
-      const int ncols = min(BN, p.vocab - col0);
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(base + (uint32_t)c0, v);
-        if (c0 >= ncols) continue;
-        const int lim = min(32, ncols - c0);
-        const int ty = tgt - col0 - c0;
-        if (ty >= 0 && ty < lim) has_y = true;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) xy = (j == ty) ? v[j] : xy;
-        float lm = v[0];
-#pragma unroll
-        for (int j = 1; j < 32; ++j) lm = j < lim ? fmaxf(lm, v[j]) : lm;
-        int excl = -1;
-        if (lm * c > Mc) {  // new top element: fold the old one in, rescale, exclude the new one
-#pragma unroll
-          for (int j = 31; j >= 0; --j) excl = (j < lim && v[j] == lm) ? j : excl;
-          const float nMc = lm * c;
-          if (Mc != -INFINITY) {
-            const float sc = ex2_approx(Mc - nMc), dl = nMc - Mc;
-            T = sc * fmaf(-dl, S, T);
-            cT = sc * fmaf(-dl, cS, cT);
-            S *= sc;
-            cS *= sc;
-            const float d = fmaf(Mx, c, -nMc), e = ex2_approx(d);
-            float y = e - cS, t = S + y;
-            cS = (t - S) - y;
-            S = t;
-            y = d * e - cT;
-            t = T + y;
-            cT = (t - T) - y;
-            T = t;
-          }
-          Mc = nMc;
-          Mx = lm;
-        }
-        float gs[4] = {0.f, 0.f, 0.f, 0.f}, gt[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (j < lim && j != excl) {
-            const float d = fmaf(v[j], c, -Mc), e = ex2_approx(d);
-            gs[j & 3] += e;
-            gt[j & 3] = fmaf(d, e, gt[j & 3]);
-          }
-        }
-        float y = ((gs[0] + gs[1]) + (gs[2] + gs[3])) - cS, t = S + y;
-        cS = (t - S) - y;
-        S = t;
-        y = ((gt[0] + gt[1]) + (gt[2] + gt[3])) - cT;
-        t = T + y;
-        cT = (t - T) - y;
-        T = t;
-      }
+      epi_tile(base, n * BN, min(BN, p.vocab - n * BN), tgt, c, a);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&tempty[acc]);
     }
-    if (grow < p.n_rows) {  // this unit's partial for (row, chunk)
-      float* o = p.part + ((size_t)grow * p.n_chunks + w.chunk) * 6;
-      o[0] = Mc;
-      o[1] = Mx;
-      o[2] = S;
-      o[3] = T;
-      o[4] = xy;
-      o[5] = has_y ? 1.f : 0.f;
-    }
+    if (grow < p.n_rows) store_partial(p, grow, w.chunk, a);  // this unit's partial for (row, chunk)
     }  // units
   }
 
@@ -309,6 +332,202 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// ---- 2-CTA variant (cta_group::2): a CTA pair computes 256-row x 256-vocab
+// logits tiles. Rank r of the pair holds rows [128 r, 128 r + 128) of the
+// tile's hidden states and vocab rows [128 r, 128 r + 128) of the W tile in
+// its shared memory; the leader (rank 0) issues tcgen05.mma.cta_group::2
+// (M256 N256 K16), which reads both CTAs' operands and writes each CTA's 128
+// accumulator rows into its own TMEM. Per CTA the shared-memory operand
+// traffic per logit halves (each W tile is loaded once per pair instead of
+// once per CTA), and one MMA instruction covers twice the work.
+constexpr int STAGES2 = 6;
+constexpr uint32_t A2_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 hidden rows
+constexpr uint32_t B2_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's half of the W tile
+constexpr uint32_t STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((2 * BM) >> 4) << 24);
+
+__device__ __forceinline__ uint32_t lm_cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t lm_cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t lm_n_clusters() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void lm_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lm_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// TMA 2-D tile into this CTA's shared memory, completing on the LEADER's mbarrier
+// (cluster address `bar_cluster`).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                                 uint32_t bar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate)
+      : "memory");
+}
+// Arrive (once the MMAs issued so far retire) on barrier `bar` in BOTH CTAs of the pair.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_lmhead2(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, const LmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A2_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);  // leader's is used
+  uint64_t* empty = full + STAGES2;                                              // both CTAs
+  uint64_t* tfull = empty + STAGES2;                                             // both CTAs
+  uint64_t* tempty = tfull + 2;                                                  // leader's is used
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = lm_cluster_ctarank();
+  const int64_t q0 = lm_cluster_id(), nq = lm_n_clusters();
+  const int64_t n_units = (int64_t)p.m_tiles * p.n_chunks;  // m_tiles counts 256-row pair tiles here
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+  }
+  lm_cluster_sync();  // both CTAs' barriers exist before any remote arrive / complete_tx
+  if (warp == 1) {    // the same warp in both CTAs: allocate 512 TMEM columns for the pair
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  lm_cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer (both CTAs) =====
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      uint32_t s = 0, ph = 0;
+      for (int64_t u = q0; u < n_units; u += nq) {
+        const Unit w = unit_of(p, u);
+        for (int n = w.t0; n < w.t1; ++n) {
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait_bounded(&empty[s], ph ^ 1);
+            const uint32_t bar = lm_mapa(smem_u32(&full[s]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
+            tma_load_2d_pair(sA + s * A2_BYTES, &tmH, kb * BK, w.m * (2 * BM) + (int)rank * BM, bar, pol);
+            tma_load_2d_pair(sB + s * B2_BYTES, &tmW, kb * BK, n * BN + (int)rank * (BN / 2), bar, pol);
+            if (++s == STAGES2) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader only) =====
+      uint32_t s = 0, ph = 0;
+      int tile = 0;
+      for (int64_t u = q0; u < n_units; u += nq) {
+        const Unit w = unit_of(p, u);
+        for (int n = w.t0; n < w.t1; ++n, ++tile) {
+          const int acc = tile & 1;
+          mbar_wait_bounded(&tempty[acc], ((tile >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d_tmem = tmem + (uint32_t)(acc * BN);
+          for (int kb = 0; kb < p.n_kb; ++kb) {
+            mbar_wait_bounded(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = umma_desc_sw128(sA + s * A2_BYTES);
+            const uint64_t bd = umma_desc_sw128(sB + s * B2_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_pair(d_tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), (kb | k) != 0);
+            umma_commit_pair(&empty[s]);  // both CTAs' stage s free once these MMAs retire
+            if (++s == STAGES2) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          umma_commit_pair(&tfull[acc]);  // both CTAs' accumulators ready
+        }
+      }
+    }
+  } else {
+    // ===== epilogue (both CTAs): one row per thread =====
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const float c = p.c;
+    const uint32_t tempty_leader0 = lm_mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = lm_mapa(smem_u32(&tempty[1]), 0);
+    int tile = 0;
+    for (int64_t u = q0; u < n_units; u += nq) {
+      const Unit w = unit_of(p, u);
+      const int64_t grow = (int64_t)w.m * (2 * BM) + (int64_t)rank * BM + row;
+      const int32_t tgt = grow < p.n_rows ? p.targets[grow] : -1;
+      RowAcc a;
+      for (int n = w.t0; n < w.t1; ++n, ++tile) {
+        const int acc = tile & 1;
+        mbar_wait_bounded(&tfull[acc], (tile >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        epi_tile(base, n * BN, min(BN, p.vocab - n * BN), tgt, c, a);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      }
+      if (grow < p.n_rows) store_partial(p, grow, w.chunk, a);
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  lm_cluster_sync();  // the peer's epilogue and the leader's MMAs are done with both TMEMs
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -343,6 +562,15 @@ __global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, i
   const float l1q = log1pf(q);
   logp[i] = (fmaf(xy, c, -Mc) - r) * kLn2 - l1q;
   if (entropy) entropy[i] = l1q + kLn2 * (fmaf(r, q, -T * ir) / (1.f + q));
+}
+
+// K6 launch mode: CTA pairs (cta_group::2) unless PRORL_K6_PAIR=0.
+bool lmhead_pair_mode() {
+  static bool pair = [] {
+    const char* e = std::getenv("PRORL_K6_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return pair;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -383,18 +611,21 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
     return fail(PRORL_E_SHAPE, "lmhead: hidden/weight must be 16-B aligned with 16-B multiple row strides");
   if (!(inv_temp > 0.f)) return fail(PRORL_E_MALFORMED_REQUEST, "lmhead: inv_temperature must be > 0");
   if (n_rows == 0) return PRORL_OK;
+  const bool pair = lmhead_pair_mode();
   CUtensorMap tmH, tmW;
   PRORL_TRY_INTERNAL(make_map(&tmH, hidden, n_rows, d, h_stride, BM));
-  PRORL_TRY_INTERNAL(make_map(&tmW, weight, vocab, d, w_stride, BN));
+  PRORL_TRY_INTERNAL(make_map(&tmW, weight, vocab, d, w_stride, pair ? BN / 2 : BN));
   LmParams p{};
   p.n_rows = n_rows;
   p.vocab = vocab;
   p.n_kb = d / BK;
   p.n_ntiles = (vocab + BN - 1) / BN;
-  p.m_tiles = (int32_t)((n_rows + BM - 1) / BM);
+  const int rows_per_tile = pair ? 2 * BM : BM;
+  p.m_tiles = (int32_t)((n_rows + rows_per_tile - 1) / rows_per_tile);
+  const int n_workers = pair ? ctx->n_sm / 2 : ctx->n_sm;  // CTA pairs or CTAs
   // Split the vocabulary into chunks so the (row tile x chunk) units balance
-  // over the SMs: pick the chunk count whose round-robin makespan
-  // ceil(units / n_sm) * tiles_per_chunk wastes the least SM time (chunks of
+  // over the workers: pick the chunk count whose round-robin makespan
+  // ceil(units / workers) * tiles_per_chunk wastes the least time (chunks of
   // >= 16 vocab tiles).
   {
     const int64_t total = (int64_t)p.m_tiles * p.n_ntiles;
@@ -404,9 +635,8 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
       if (nch > 1 && tpc < 16) break;  // keep partial-merge traffic small (<= 1/16 of the tiles)
       const int32_t chunks = (p.n_ntiles + tpc - 1) / tpc;
       const int64_t units = (int64_t)p.m_tiles * chunks;
-      const int64_t g = std::min<int64_t>(units, ctx->n_sm);
-      const double eff = (double)total / ((double)g * (double)((units + g - 1) / g) * tpc) *
-                         ((double)g / ctx->n_sm);
+      const int64_t g = std::min<int64_t>(units, n_workers);
+      const double eff = (double)total / ((double)g * (double)((units + g - 1) / g) * tpc) * ((double)g / n_workers);
       if (eff > best + 1e-3) {
         best = eff;
         p.tpc = tpc;
@@ -418,11 +648,29 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
   p.targets = targets;
   PRORL_CUDA(ctx->lm_part.ensure(sizeof(float) * 6 * (size_t)n_rows * (size_t)p.n_chunks));
   p.part = ctx->lm_part.as<float>();
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
-  PRORL_CUDA(cudaFuncSetAttribute(k_lmhead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t units = (int64_t)p.m_tiles * p.n_chunks;
-  const unsigned grid = (unsigned)std::min<int64_t>(units, ctx->n_sm);
-  k_lmhead<<<grid, kThreads, smem, st>>>(tmH, tmW, p);
+  if (pair) {
+    const size_t smem = (size_t)STAGES2 * STAGE2_BYTES + 1024 + 256;
+    PRORL_CUDA(cudaFuncSetAttribute(k_lmhead2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(units, n_workers)));
+    PRORL_CUDA(cudaLaunchKernelEx(&cfg, k_lmhead2, tmH, tmW, p));
+  } else {
+    const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+    PRORL_CUDA(cudaFuncSetAttribute(k_lmhead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = (unsigned)std::min<int64_t>(units, n_workers);
+    k_lmhead<<<grid, kThreads, smem, st>>>(tmH, tmW, p);
+  }
   PRORL_CUDA(cudaGetLastError());
   k_lmhead_merge<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(p.part, n_rows, p.n_chunks, p.c, logp, entropy);
   PRORL_CUDA(cudaGetLastError());
