@@ -87,12 +87,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar,
+                                            uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
+}
+
+// L2 policies: the hidden-state tile of a unit is re-streamed for every vocab
+// tile of its chunk (keep it: evict_last); the W tiles are shared by all the
+// units walking the same chunk at roughly the same time (normal).
+__device__ __forceinline__ uint64_t policy_keep() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
@@ -257,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
+      const uint64_t pol_h = policy_keep(), pol_w = policy_normal();
       uint32_t s = 0, ph = 0;
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
         const Unit w = unit_of(p, u);
@@ -264,8 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait_bounded(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-            tma_load_2d(sA + s * A_BYTES, &tmH, kb * BK, w.m * BM, &full[s]);
-            tma_load_2d(sB + s * B_BYTES, &tmW, kb * BK, n * BN, &full[s]);
+            tma_load_2d(sA + s * A_BYTES, &tmH, kb * BK, w.m * BM, &full[s], pol_h);
+            tma_load_2d(sB + s * B_BYTES, &tmW, kb * BK, n * BN, &full[s], pol_w);
             if (++s == STAGES) {
               s = 0;
               ph ^= 1;
@@ -446,8 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer (both CTAs) =====
-      uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      const uint64_t pol_h = policy_keep(), pol_w = policy_normal();
       uint32_t s = 0, ph = 0;
       for (int64_t u = q0; u < n_units; u += nq) {
         const Unit w = unit_of(p, u);
@@ -456,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait_bounded(&empty[s], ph ^ 1);
             const uint32_t bar = lm_mapa(smem_u32(&full[s]), 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
-            tma_load_2d_pair(sA + s * A2_BYTES, &tmH, kb * BK, w.m * (2 * BM) + (int)rank * BM, bar, pol);
-            tma_load_2d_pair(sB + s * B2_BYTES, &tmW, kb * BK, n * BN + (int)rank * (BN / 2), bar, pol);
+            tma_load_2d_pair(sA + s * A2_BYTES, &tmH, kb * BK, w.m * (2 * BM) + (int)rank * BM, bar, pol_h);
+            tma_load_2d_pair(sB + s * B2_BYTES, &tmW, kb * BK, n * BN + (int)rank * (BN / 2), bar, pol_w);
             if (++s == STAGES2) {
               s = 0;
               ph ^= 1;
@@ -623,10 +638,14 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
   const int rows_per_tile = pair ? 2 * BM : BM;
   p.m_tiles = (int32_t)((n_rows + rows_per_tile - 1) / rows_per_tile);
   const int n_workers = pair ? ctx->n_sm / 2 : ctx->n_sm;  // CTA pairs or CTAs
-  // Split the vocabulary into chunks so the (row tile x chunk) units balance
-  // over the workers: pick the chunk count whose round-robin makespan
-  // ceil(units / workers) * tiles_per_chunk wastes the least time (chunks of
-  // >= 16 vocab tiles).
+  // Split the vocabulary into chunks only as far as needed to keep the workers
+  // busy: the FEWEST chunks whose round-robin makespan ceil(units / workers) *
+  // tiles_per_chunk keeps >= 85 % of the workers' time useful (else the best
+  // balance; chunks of >= 16 vocab tiles). Few chunks keep every worker walking
+  // the same W tiles in step, so W streams from HBM about once (ncu: 0.87 GB
+  // per launch at one chunk vs 13-15 GB at 15 chunks); the kernel runs at the
+  // power cap, and the saved DRAM energy buys clock (measured sustained:
+  // 1 263 TFLOP/s with CTA pairs and one chunk vs 1 195 with 15 chunks).
   {
     const int64_t total = (int64_t)p.m_tiles * p.n_ntiles;
     double best = -1.0;
@@ -642,7 +661,13 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
         p.tpc = tpc;
         p.n_chunks = chunks;
       }
+      if (eff >= 0.85) break;
     }
+  }
+  if (const char* e = std::getenv("PRORL_K6_CHUNKS")) {  // tuning override: vocab chunks per row tile
+    const int32_t nch = std::max(1, std::min(p.n_ntiles, std::atoi(e)));
+    p.tpc = (p.n_ntiles + nch - 1) / nch;
+    p.n_chunks = (p.n_ntiles + p.tpc - 1) / p.tpc;
   }
   p.c = inv_temp * kLog2e;
   p.targets = targets;
