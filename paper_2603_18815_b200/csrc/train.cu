@@ -22,9 +22,13 @@
 //     partials meet in shared memory after one named barrier and every warp
 //     merges them with the same fixed tree, so all hold bit-identical lse /
 //     logp / loss terms.
-//   * Pass B (gradient): the producer streams the same row again — from L2
-//     (evict_first) — and the warps write grad = s (1[v = y] - p_v) as 16-B
-//     streaming stores. The producer runs ahead across passes and rows.
+//   * Pass B (gradient): the last ring-full of pass-A pieces is still in
+//     shared memory and is consumed first, straight from there (pass A holds
+//     those slots); the rest of the row is streamed again — from L2
+//     (evict_first) — into the slots they free. Warps write
+//     grad = s (1[v = y] - p_v) as 16-B streaming stores. The producer runs
+//     ahead across passes and rows. (Rows of <= 192 KB never leave shared
+//     memory between the passes.)
 //   * One lane per group keeps the loss epilogue (fp64 partials + per-turn
 //     buckets, fixed order); the groups' sums merge in fixed order into one
 //     slab row per CTA (deterministic).
@@ -180,9 +184,8 @@ struct RowGeo {
 };
 
 template <int ES, int kUnit>
-__device__ __forceinline__ RowGeo row_geo(const TrainArgs& p, int64_t i) {
+__device__ __forceinline__ RowGeo row_geo(const TrainArgs& p, int64_t r) {
   RowGeo g;
-  const int64_t r = p.rows ? (int64_t)p.rows[i] : i;
   g.rp = p.logits + r * p.stride_bytes;
   const uintptr_t st = reinterpret_cast<uintptr_t>(g.rp);
   const uintptr_t en = st + (uintptr_t)p.vocab * ES;
@@ -261,9 +264,10 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t pc = 0;
       for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x) {
-        const RowGeo g = row_geo<ES, kUnit>(p, i);
+        const RowGeo g = row_geo<ES, kUnit>(p, p.rows ? (int64_t)p.rows[i] : i);
+        const int fh = max(0, g.npc - kRG);  // pieces [fh, npc) stay in the ring for pass B
         for (int pass = 0; pass < 2; ++pass) {
-          for (int k = 0; k < g.npc; ++k, ++pc) {
+          for (int k = 0; k < (pass == 0 ? g.npc : fh); ++k, ++pc) {
             const int s = (int)(pc % kRG);
             mbar_wait_t(&empty[s], ((pc / kRG) & 1) ^ 1);
             const uint32_t bytes = min((uint32_t)kPiece, g.nb - (uint32_t)k * kPiece);
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
   uint32_t pcb = 0;  // ring piece counter at the start of the row
   uint32_t j = 0;    // rows done by this CTA
   for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x, ++j) {
-    const RowGeo g = row_geo<ES, kUnit>(p, i);
+    const RowGeo g = row_geo<ES, kUnit>(p, p.rows ? (int64_t)p.rows[i] : i);
     const int32_t y = p.targets[i];
     float xy = 0.f, old = 0.f, A = 0.f, ref = 0.f;
     if (lane == 0) {
@@ -304,6 +308,10 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
     // first piece (offset from pc0) of a pass that this warp consumes
     auto first_piece = [&](uint32_t pc0) { return (int)(((uint32_t)(wq / kSplit) + kPG - pc0 % kPG) % kPG); };
 
+    // pieces [fh, npc) — the last ring-full of pass A — are held in shared
+    // memory and re-read by pass B from there; only [0, fh) is streamed again
+    const int fh = max(0, g.npc - kRG);
+
     // ---- pass A: statistics ----
     Top top{-INFINITY, 0.f};
     float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -313,11 +321,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
       const int u = k * kSplit + kk;
       const int s = (int)(pc % kRG);
       mbar_wait_t(&full[s], (pc / kRG) & 1);
-      if (u >= g.nsub) {  // padding unit of the pass's last piece
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
-        continue;
-      }
+      if (u >= g.nsub) continue;  // padding unit of the (held) last piece: released in pass B
       const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
       const uint32_t nvv = min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) >> 4;
       uint4 v[kNV];
@@ -331,8 +335,10 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
           v[jj] = qv < nvv ? sv[qv] : fill;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+      if (k < fh) {  // streamed piece: free the slot; held pieces are released by pass B
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+      }
 #pragma unroll
       for (int g0 = 0; g0 < kNV; g0 += SUBV) {
         uint4 w[SUBV];
@@ -437,39 +443,47 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
     const bool y_in = yb >= g.a && yb < g.a + g.nb;
     const int32_t yvec = y_in ? (int32_t)((yb - g.a) >> 4) : -1;
     const int ye = (int)((yb & 15) / ES);
-    const uint32_t pcB = pcb + (uint32_t)g.npc;
-    for (int k = first_piece(pcB); k < g.npc; k += kPG) {
-      const uint32_t pc = pcB + (uint32_t)k;
-      const int u = k * kSplit + kk;
-      const int s = (int)(pc % kRG);
-      mbar_wait_t(&full[s], (pc / kRG) & 1);
-      if (u >= g.nsub) {  // padding unit of the pass's last piece
+    const uint32_t pcB = pcb + (uint32_t)g.npc;  // ring position of the first re-streamed piece
+    // held pieces [fh, npc) (already in the ring, mapped by their pass-A slot),
+    // then the re-streamed pieces [0, fh)
+    int k = first_piece(pcb);
+    if (k < fh) k += (fh - k + kPG - 1) / kPG * kPG;
+    for (int held = 1; held >= 0; --held) {
+      if (!held) k = first_piece(pcB);
+      const int kend = held ? g.npc : fh;
+      for (; k < kend; k += kPG) {
+        const uint32_t pc = (held ? pcb : pcB) + (uint32_t)k;
+        const int u = k * kSplit + kk;
+        const int s = (int)(pc % kRG);
+        if (!held) mbar_wait_t(&full[s], (pc / kRG) & 1);
+        if (u >= g.nsub) {  // padding unit of the last piece
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+          continue;
+        }
+        const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
+        const uint32_t nvv = min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) >> 4;
+        const int32_t tq = y_in ? yvec - u * (kUnit / 16) : -1;  // target vector inside this unit
+        uint4* dst = reinterpret_cast<uint4*>(g.a + (uintptr_t)u * kUnit + (uintptr_t)p.goff);
+        uint4 v[kNV];
+#pragma unroll
+        for (int jj = 0; jj < kNV; ++jj) {
+          const uint32_t qv = lane + 32 * jj;
+          v[jj] = qv < nvv ? sv[qv] : make_uint4(0, 0, 0, 0);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
-        continue;
-      }
-      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
-      const uint32_t nvv = min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) >> 4;
-      const int32_t tq = y_in ? yvec - u * (kUnit / 16) : -1;  // target vector inside this unit
-      uint4* dst = reinterpret_cast<uint4*>(g.a + (uintptr_t)u * kUnit + (uintptr_t)p.goff);
-      uint4 v[kNV];
 #pragma unroll
-      for (int jj = 0; jj < kNV; ++jj) {
-        const uint32_t qv = lane + 32 * jj;
-        v[jj] = qv < nvv ? sv[qv] : make_uint4(0, 0, 0, 0);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
-#pragma unroll
-      for (int jj = 0; jj < kNV; ++jj) {
-        const uint32_t qv = lane + 32 * jj;
-        if (qv < nvv) {
-          uint4 o = make_uint4(0, 0, 0, 0);
-          if (!zero) {
-            o = GElem<T>::vec(v[jj], c2, nl2, s2);
-            if ((int32_t)qv == tq) o = patch_target<T>(o, ye, gy);
+        for (int jj = 0; jj < kNV; ++jj) {
+          const uint32_t qv = lane + 32 * jj;
+          if (qv < nvv) {
+            uint4 o = make_uint4(0, 0, 0, 0);
+            if (!zero) {
+              o = GElem<T>::vec(v[jj], c2, nl2, s2);
+              if ((int32_t)qv == tq) o = patch_target<T>(o, ye, gy);
+            }
+            __stcs(dst + qv, o);
           }
-          __stcs(dst + qv, o);
         }
       }
     }
@@ -484,7 +498,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
         else reinterpret_cast<float*>(gp)[idx] = gv;
       }
     }
-    pcb += 2u * (uint32_t)g.npc;
+    pcb += (uint32_t)(g.npc + fh);
   }
 
   // ---- slab row of this CTA: the groups' sums in fixed order ----
