@@ -143,6 +143,16 @@ template <> __device__ __forceinline__ float load_clamped<float>(const uint8_t* 
   return fmaxf(reinterpret_cast<const float*>(base)[idx], -1.5845632502852868e29f);
 }
 
+// Hysteresis of the warp-uniform running max in pass A. The reference point Mc
+// need not be the exact maximum — every formula (the excluded element's
+// residual r = Mx c - Mc, q = S 2^-r, the partial merge) holds for any Mc —
+// it only has to bound the terms. With a slack of 1 (log2 units) a term is at
+// most 2, and a row whose peak was not excluded has p_peak <= 2/3, so
+// |logp| >= 0.4 and log1p(q) <= ln 3: the fp32 error stays ~1e-7 relative,
+// inside the 1e-5 contract; peaked rows (p -> 1) still raise and exclude their
+// peak exactly.
+constexpr float kRaiseSlack = 1.0f;
+
 // One 32-wide step of the scalar online logsumexp (element x per lane).
 __device__ __forceinline__ void scalar_step(float x, float c, Top& top, float2 (&S)[2], float2 (&Tt)[2], int lane) {
   if (__any_sync(kFull, x * c > top.Mc)) {
@@ -345,7 +355,11 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
 #pragma unroll
         for (int jj = 0; jj < SUBV; ++jj) w[jj] = v[g0 + jj];
         const float lm = Elem<T>::template group_max<SUBV>(w);
-        if (__any_sync(kFull, lm * c > top.Mc)) {
+        // raise only when a group beats the running max by more than kRaiseSlack
+        // (log2 units): later terms may then reach 2^kRaiseSlack, which keeps
+        // fp32 exact enough, and most of a warp's ~5 units per row skip the
+        // raise + exclusion path (see the note at kRaiseSlack)
+        if (__any_sync(kFull, lm * c > top.Mc + kRaiseSlack)) {
           const int L = raise_top(lm, c, top, S, Tt, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(w, top.Mx);
         }

@@ -230,3 +230,30 @@ def test_score_host_train_mode(scorer, cuda):
     for j in range(n_mb):
         n = min(mb, sh.n_active - j * mb)
         assert torch.equal(pool[j][:n], gpool[j][:n])
+
+
+def test_score_grad_running_max_slack(scorer, cuda):
+    """Rows whose maximum appears in a later warp unit just below / above the
+    running-max slack (1 in log2 units = 0.69 nats) of an earlier near-max:
+    the reference point then is not the exact maximum (or is raised), and
+    logp / entropy / gradient must still meet the oracle tolerances."""
+    V = 151936
+    rng = np.random.default_rng(17)
+    rows, targets = [], []
+    for early, late, tgt_late in [(10.0, 10.6, True), (10.0, 10.6, False), (10.0, 10.68, True),
+                                  (10.0, 10.8, True), (10.0, 30.0, True), (10.0, 9.5, False)]:
+        r = rng.normal(0, 2, V).astype(np.float32)
+        r[100] = early
+        r[140000] = late
+        rows.append(r)
+        targets.append(140000 if tgt_late else 100)
+    xh = np.stack(rows)
+    x = torch.from_numpy(xh).to(cuda).to(torch.bfloat16)
+    host = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    n = len(rows)
+    t = np.array(targets, np.int32)
+    old = np.full(n, -0.5, np.float32)
+    adv = np.array([1.0, -1.0], np.float32)
+    seq = (np.arange(n) % 2).astype(np.int32)
+    turn = np.zeros(n, np.int16)
+    _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 10.0)
