@@ -14,6 +14,9 @@
 //     chunk is pulled into registers with LDS.128 and its stage released at
 //     once;
 //   * online base-2 logsumexp with a WARP-UNIFORM running max Mc of x*c
+//     (raised only when a group beats it by more than 1 in log2 units — the
+//     reference point need not be the exact max, see train.cu kRaiseSlack —
+//     which skips most raises: +1.2 % at C2)
 //     (c = inv_temp * log2 e): per group of SUBV*8 bf16 per lane a packed
 //     max (HMNMX2) and one vote decide whether the max moved; only then (a
 //     handful of times per row) does the warp take the rescale path, so the
@@ -30,6 +33,7 @@
 //     packed min.u16x2 per two logits (they then contribute exactly 0);
 //   * unaligned row heads/tails (V*esz not a multiple of 16 B, odd row
 //     offsets) are read by lanes directly, the aligned interior goes via TMA.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -92,6 +96,7 @@ struct ScoreArgs {
   float* entropy;
   double* slab;
   int accumulate;
+  float raise_slack;  // running-max hysteresis in log2 units (PRORL_K2_SLACK; see train.cu kRaiseSlack)
 };
 
 // Block-level merge of per-warp partials (fixed warp order) into slab row b.
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
 #pragma unroll
         for (int j = 0; j < SUBV; ++j) u[j] = v[g0 + j];
         const float lm = Elem<T>::template group_max<SUBV>(u);
-        if (__any_sync(kFull, lm * c > top.Mc)) {
+        if (__any_sync(kFull, lm * c > top.Mc + p.raise_slack)) {
           const int L = raise_top(lm, c, top, S, Tt, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(u, top.Mx);
         }
@@ -413,6 +418,11 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.entropy = entropy;
   a.slab = slab;
   a.accumulate = accumulate ? 1 : 0;
+  static const float slack = [] {
+    const char* e = std::getenv("PRORL_K2_SLACK");
+    return e ? std::max(0.f, std::min(1.f, (float)std::atof(e))) : 1.f;  // measured +1.2 % at C2 (power-capped)
+  }();
+  a.raise_slack = slack;
   if (cfg) {
     a.lo_bound = 1.0f - cfg->eps_lo;
     a.hi_bound = 1.0f + cfg->eps_hi;

@@ -257,3 +257,8 @@ def test_score_grad_running_max_slack(scorer, cuda):
     seq = (np.arange(n) % 2).astype(np.int32)
     turn = np.zeros(n, np.int16)
     _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 10.0)
+    # K2 uses the same running-max slack: forward-only logp / entropy on the same rows
+    lp, ent = scorer.logprob_entropy(x, dev(t, cuda))
+    olp, oent = O.logprob_entropy(host, t)
+    assert_rows_close(lp.cpu().numpy(), olp, "K2 logp")
+    assert_rows_close(ent.cpu().numpy(), oent, "K2 entropy")
