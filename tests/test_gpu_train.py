@@ -262,3 +262,23 @@ def test_score_grad_running_max_slack(scorer, cuda):
     olp, oent = O.logprob_entropy(host, t)
     assert_rows_close(lp.cpu().numpy(), olp, "K2 logp")
     assert_rows_close(ent.cpu().numpy(), oent, "K2 entropy")
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_score_grad_randomized_layouts(scorer, cuda, case):
+    """Seeded random layouts (vocab, row padding, dtype, rows indirection, in
+    place, KL) through K7 vs the fp64 oracle."""
+    rng = np.random.default_rng(1000 + case)
+    dtype = "bf16" if rng.random() < 0.7 else "fp32"
+    V = int(rng.choice([int(rng.integers(2, 300)), int(rng.integers(300, 20000)), int(rng.integers(20000, 200000))]))
+    pad = int(rng.integers(0, 9)) if rng.random() < 0.5 else 0
+    n = int(rng.integers(1, 40 if V > 50000 else 120))
+    x, host, t, old, adv, seq, turn = _case(scorer, cuda, V, n, dtype, stride=V + pad, seed=case, n_seq=5)
+    rows = rng.permutation(n).astype(np.int32) if rng.random() < 0.5 else None
+    cfg, ref = None, None
+    if rng.random() < 0.4:
+        cfg = LossConfig(kl_coef=0.1)
+        lp0, _ = scorer.logprob_entropy(x, dev(t, cuda), rows=None if rows is None else dev(rows, cuda), vocab=V)
+        ref = (lp0.cpu().numpy() + rng.normal(0, 0.3, n)).astype(np.float32)
+    _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, float(n * 3), rows=rows, cfg=cfg, ref=ref,
+               inplace=rows is None and rng.random() < 0.5)
