@@ -15,6 +15,16 @@
  *                                  (proj/src/trainer/harness.cpp:84-102)
  *   prorl_logprob_entropy new      (absent in reference: SPEC.md:8)
  *   prorl_clipped_loss    new      (absent in reference: SPEC.md:741; DAPO PAPER.md:368)
+ *   prorl_score_rows      new      K2+K4 fused (same sources as the two above)
+ *   prorl_logits_grad     new      backward of the DAPO surrogate
+ *                                  through the log-softmax (SURVEY §8 f rank 1)
+ *   prorl_score_grad      new      score_rows + logits_grad in one kernel (K7)
+ *   prorl_lmhead_logprob  new      fused LM head + logprob (SURVEY §8 f rank 2;
+ *                                  the model forward is outside SPEC.md:8)
+ *   prorl_ingest_responses replaces the response parse that drops the
+ *                                  trajectory (proj/src/trainer/harness.cpp:
+ *                                  254-273), schema of proj/src/handlers.cpp:57-91
+ *   prorl_synth_rewards   restates generate_workload (proj/src/trainer/workload.cpp:62-107)
  *   prorl_allreduce       new      (the reference has no collectives)
  *   prorl_score_host      replaces the trajectory drop at
  *                                  proj/src/trainer/harness.cpp:263-273 — the
