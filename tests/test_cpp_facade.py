@@ -97,3 +97,13 @@ def test_cpp_score_responses_tool_vs_oracle(tmp_path):
     for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM, N.P_KL1_SUM):
         assert abs(got[i] - P[i]) <= 1e-5 * Q[i], (i, got[i], P[i])
     assert got[N.P_N_ACTIVE] == P[N.P_N_ACTIVE] and got[N.P_N_ROLLOUTS] == P[N.P_N_ROLLOUTS]
+    assert d["grad_batches"] == 0
+    # --train: the K7 training step through the facade, same metrics, one gradient hand-off per micro-batch
+    r = subprocess.run([str(exe), str(path), "4", "32000", "fp32", "21", "--train"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    got = np.array(d["partials"])
+    for i in (N.P_LOSS_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM, N.P_RATIO_SUM, N.P_KL1_SUM):
+        assert abs(got[i] - P[i]) <= 1e-5 * Q[i], (i, got[i], P[i])
+    assert d["grad_rows"] == sh.n_active and d["grad_batches"] == -(-sh.n_active // 4096)
