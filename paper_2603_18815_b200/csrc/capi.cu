@@ -260,7 +260,7 @@ int prorl_score_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_st
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                      float inv_temp, const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy,
                      double* partials_dev, void* grad, int64_t grad_stride, float* dlogp, void* stream) {
-  if (!c || !cfg || !grad) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_grad: null ctx/cfg/grad");
+  if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_grad: null ctx/cfg");
   if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "score_grad: unknown dtype");
   if (vocab <= 0 || row_stride < vocab) return fail(PRORL_E_SHAPE, "score_grad: need vocab > 0, row_stride >= vocab");
   if (grad_stride != row_stride)
@@ -268,12 +268,14 @@ int prorl_score_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_st
   if (!(inv_temp > 0.f) || !(n_global > 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "score_grad: bad inv_temp/n_global");
   if (cfg->n_buckets < 1 || cfg->n_buckets > PRORL_TURN_BUCKETS)
     return fail(PRORL_E_SHAPE, "score_grad: n_buckets out of [1, 64]");
+  if (n_rows <= 0) return PRORL_OK;
+  if (!logits || !grad || !targets || !old_lp || !adv || !row_seq || !row_turn)
+    return fail(PRORL_E_MALFORMED_REQUEST, "score_grad: null logits/grad/targets/old_lp/adv/row_seq/row_turn");
   const int esz = dtype == PRORL_BF16 ? 2 : 4;
   const intptr_t delta = static_cast<const uint8_t*>(grad) - static_cast<const uint8_t*>(logits);
   if (reinterpret_cast<uintptr_t>(logits) % esz || (delta % 16) != 0)
     return fail(PRORL_E_SHAPE, "score_grad: grad must have the logits' 16-byte alignment phase");
   PRORL_CUDA(cudaSetDevice(c->device));
-  if (n_rows <= 0) return PRORL_OK;
   const int slab_rows = train_slab_rows(c);
   PRORL_CUDA(c->slab.ensure(sizeof(double) * PRORL_N_PARTIALS * (size_t)std::max(slab_rows, loss_slab_rows(c))));
   int used = 0;

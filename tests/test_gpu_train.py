@@ -282,3 +282,28 @@ def test_score_grad_randomized_layouts(scorer, cuda, case):
         ref = (lp0.cpu().numpy() + rng.normal(0, 0.3, n)).astype(np.float32)
     _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, float(n * 3), rows=rows, cfg=cfg, ref=ref,
                inplace=rows is None and rng.random() < 0.5)
+
+
+def test_score_grad_errors(scorer, cuda):
+    """Layout / argument errors surface as rollout error codes, nothing launches."""
+    from paper_2603_18815_b200.hotpath import RolloutError
+    x = torch.zeros((4, 64), dtype=torch.bfloat16, device=cuda)
+    t = torch.zeros(4, dtype=torch.int32, device=cuda)
+    f = torch.zeros(4, dtype=torch.float32, device=cuda)
+    tr = torch.zeros(4, dtype=torch.int16, device=cuda)
+    with pytest.raises(RolloutError) as e:   # gradient with another row stride
+        scorer.score_grad(x, t, f, f, t, tr, 10.0, grad=torch.zeros((4, 72), dtype=torch.bfloat16, device=cuda))
+    assert e.value.code == "shape_mismatch"
+    with pytest.raises(RolloutError) as e:   # gradient with another 16-B phase
+        buf = torch.zeros(4 * 64 + 1, dtype=torch.bfloat16, device=cuda)
+        scorer.score_grad(x, t, f, f, t, tr, 10.0, grad=buf[1:].view(4, 64))
+    assert e.value.code == "shape_mismatch"
+    with pytest.raises(RolloutError) as e:   # no active rows in the global count
+        scorer.score_grad(x, t, f, f, t, tr, 0.0)
+    assert e.value.code == "malformed_request"
+    with pytest.raises(RolloutError) as e:   # missing row arrays
+        scorer.score_grad(x, t, None, f, t, tr, 10.0)
+    assert e.value.code == "malformed_request"
+    # zero rows: a no-op that leaves the partials untouched
+    part, *_ = scorer.score_grad(x[:0], t[:0], f[:0], f, t[:0], tr[:0], 10.0)
+    assert float(part.abs().sum()) == 0.0
