@@ -335,6 +335,14 @@ typedef int (*prorl_hidden_fn)(void* user, int64_t row0, int64_t n, const int32_
  * (the LM-head backward of the trainer); a non-zero return aborts the step. */
 typedef int (*prorl_grad_fn)(void* user, int64_t row0, int64_t n, const void* d_grad, int64_t row_stride,
                              void* stream);
+/* Reference-policy logprobs for the k3 KL term (cfg->loss.kl_coef,
+ * PAPER.md:386): for each micro-batch, a device array of n fp32 logprobs of the
+ * rows' targets under the reference policy (rows as for prorl_logits_fn),
+ * stream-ordered on `stream`. prorl_score_host rejects kl_coef != 0 without
+ * provide_ref (the term would silently vanish otherwise). */
+typedef int (*prorl_ref_fn)(void* user, int64_t row0, int64_t n, const int32_t* d_rows, const int32_t* d_seq,
+                            const int32_t* d_cu_seqlens, const int32_t* d_targets, const float** d_ref_lp,
+                            void* stream);
 typedef struct prorl_logits_pool {
   void* const* buffers; int32_t n_pool; int32_t fill; int64_t row_stride;
   uint64_t seed; float sigma; int32_t pad_;
@@ -342,6 +350,7 @@ typedef struct prorl_logits_pool {
   prorl_hidden_fn provide_hidden; const void* weight; int64_t w_stride; int32_t d_model; int32_t pad2_;
   int32_t train; int32_t pad3_; double n_global;
   void* const* grad_buffers; prorl_grad_fn consume_grad; void* grad_user;
+  prorl_ref_fn provide_ref; void* ref_user;
 } prorl_logits_pool;
 
 /* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for

@@ -75,6 +75,14 @@ class LogitsSource {
                              const std::int32_t* d_seq, const std::int32_t* d_cu_seqlens,
                              const std::int32_t* d_targets, const float* d_old_lp, std::int64_t* row_stride,
                              void* stream) = 0;
+  // Reference-policy logprobs of the same rows' targets (device, n floats) for
+  // the k3 KL term (ScoreConfig::kl_coef). Needed only when
+  // kl_coef != 0; the default has none (the step then throws MalformedRequest).
+  virtual const float* ref_logprobs(std::int64_t /*row0*/, std::int64_t /*n*/, const std::int32_t* /*d_rows*/,
+                                    const std::int32_t* /*d_seq*/, const std::int32_t* /*d_cu_seqlens*/,
+                                    const std::int32_t* /*d_targets*/, void* /*stream*/) {
+    return nullptr;
+  }
 };
 
 // The LM-head backward: receives dL/dlogits of one micro-batch (active rows

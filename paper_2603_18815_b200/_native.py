@@ -68,7 +68,10 @@ class LogitsPool(C.Structure):
                 ("seed", C.c_uint64), ("sigma", C.c_float), ("pad_", C.c_int32), ("provide", vp), ("user", vp),
                 ("provide_hidden", vp), ("weight", vp), ("w_stride", C.c_int64), ("d_model", C.c_int32),
                 ("pad2_", C.c_int32), ("train", C.c_int32), ("pad3_", C.c_int32), ("n_global", C.c_double),
-                ("grad_buffers", vp), ("consume_grad", vp), ("grad_user", vp)]
+                ("grad_buffers", vp), ("consume_grad", vp), ("grad_user", vp), ("provide_ref", vp), ("ref_user", vp)]
+
+# prorl_ref_fn
+REF_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int64, C.c_int64, vp, vp, vp, vp, C.POINTER(vp), vp)
 
 # prorl_grad_fn
 GRAD_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int64, C.c_int64, vp, C.c_int64, vp)

@@ -117,7 +117,7 @@ static_assert(sizeof(prorl_packed) == 13 * 8, "prorl_packed layout");
 static_assert(sizeof(prorl_loss_cfg) == 16, "prorl_loss_cfg layout");
 static_assert(sizeof(prorl_score_cfg) == 40, "prorl_score_cfg layout");
 static_assert(sizeof(prorl_host_batch) == 88, "prorl_host_batch layout");
-static_assert(sizeof(prorl_logits_pool) == 128, "prorl_logits_pool layout");
+static_assert(sizeof(prorl_logits_pool) == 144, "prorl_logits_pool layout");
 static_assert(sizeof(prorl_ingest_result) == 112, "prorl_ingest_result layout");
 
 extern "C" {
@@ -426,6 +426,8 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: lm-head mode needs weight and d_model");
   if (cfg->microbatch_rows < 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: microbatch_rows < 1");
   const bool train_mode = pool->train != 0;
+  if (cfg->loss.kl_coef != 0.f && !pool->provide_ref)
+    return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: kl_coef != 0 needs provide_ref (reference logprobs)");
   if (train_mode && lmhead_mode)
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: training mode needs the logits path (no fused LM head)");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
@@ -537,6 +539,15 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   const double n_global = pool->n_global > 0.0 ? pool->n_global : (double)std::max<int64_t>(A, 1);
   for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
     const int64_t n = std::min(mb, A - row0);
+    const float* ref_lp = nullptr;  // k3 KL reference logprobs of this micro-batch
+    if (pool->provide_ref && cfg->loss.kl_coef != 0.f) {
+      const int rc = pool->provide_ref(pool->ref_user, row0, n, pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
+                                       pk.act_target + row0, &ref_lp, stream);
+      if (rc != PRORL_OK)
+        return fail(rc, "prorl_score_host: reference-logprob callback failed with status " + std::to_string(rc) +
+                            " at micro-batch " + std::to_string(j));
+      if (!ref_lp) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: reference-logprob callback returned null");
+    }
     if (lmhead_mode) {
       const void* hid = nullptr;
       int64_t hs = pool->d_model;
@@ -552,7 +563,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
                               pk.act_target + row0, n, cfg->inv_temperature, lp, en, st));
       int used = 0;
       PRORL_TRY(launch_loss(c, lp, en, pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0,
-                            pk.act_turn + row0, nullptr, n, &cfg->loss, slab, loss_slab_rows(c), &used, st));
+                            pk.act_turn + row0, ref_lp, n, &cfg->loss, slab, loss_slab_rows(c), &used, st));
       PRORL_TRY(launch_slab_reduce(slab, used, partials, st));
       continue;
     }
@@ -584,7 +595,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
         return fail(PRORL_E_SHAPE, "prorl_score_host: gradient buffer must share the logits' 16-byte phase");
       int used = 0;
       PRORL_TRY(launch_train(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
-                             pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr,
+                             pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp,
                              n, cfg->inv_temperature, &cfg->loss, n_global, nullptr, nullptr, nullptr, grad, slab, true,
                              &used, st));
       if (pool->consume_grad) {
@@ -596,7 +607,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
       continue;
     }
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
-                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, nullptr, n,
+                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
   }
   if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));

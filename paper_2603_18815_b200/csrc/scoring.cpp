@@ -223,6 +223,22 @@ prorl_score_cfg to_c(const ScoreConfig& cfg) {
   c.microbatch_rows = cfg.microbatch_rows;
   return c;
 }
+int provide_ref(void* user, std::int64_t row0, std::int64_t n, const std::int32_t* d_rows, const std::int32_t* d_seq,
+                const std::int32_t* d_cu_seqlens, const std::int32_t* d_targets, const float** d_ref_lp,
+                void* stream) {
+  auto* t = static_cast<Trampoline*>(user);
+  try {
+    *d_ref_lp = t->src->ref_logprobs(row0, n, d_rows, d_seq, d_cu_seqlens, d_targets, stream);
+    if (*d_ref_lp) return PRORL_OK;
+    t->error = "kl_coef != 0 but the logits source provides no reference logprobs";
+  } catch (const Error& e) {
+    t->error = e.code() + ": " + e.what();
+  } catch (const std::exception& e) {
+    t->error = e.what();
+  }
+  t->status = PRORL_E_MALFORMED_REQUEST;
+  return t->status;
+}
 }  // namespace
 
 ScoreResult DeviceScorer::score_batch(const HostBatch& batch, LogitsSource& logits, const ScoreConfig& cfg,
@@ -253,6 +269,10 @@ ScoreResult DeviceScorer::score_view(const prorl_host_batch& hb, LogitsSource& l
   prorl_logits_pool pool{};
   pool.provide = &provide_logits;
   pool.user = &tr;
+  if (cfg.kl_coef != 0.f) {
+    pool.provide_ref = &provide_ref;
+    pool.ref_user = &tr;
+  }
   double partials[PRORL_N_PARTIALS];
   float tm[5];
   const int st = prorl_score_host(ctx_, &hb, &c, &pool, partials, tm, stream);
@@ -276,6 +296,10 @@ ScoreResult DeviceScorer::train_view(const prorl_host_batch& hb, LogitsSource& l
   prorl_logits_pool pool{};
   pool.provide = &provide_logits;
   pool.user = &tr;
+  if (cfg.kl_coef != 0.f) {
+    pool.provide_ref = &provide_ref;
+    pool.ref_user = &tr;
+  }
   pool.train = 1;
   pool.n_global = n_global;
   pool.consume_grad = &consume_grad;

@@ -252,7 +252,7 @@ class Scorer:
         dummy = (C.c_void_p * 1)(None)
         lp = N.LogitsPool(C.cast(dummy, C.c_void_p), 0, 0, 0, 0, 0.0, 0, None, None,
                           C.cast(fn, C.c_void_p), ptr(weight), weight.stride(0), weight.shape[1], 0,
-                          0, 0, 0.0, None, None, None)
+                          0, 0, 0.0, None, None, None, None, None)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()
@@ -263,7 +263,7 @@ class Scorer:
     # ---- whole per-GPU step from host buffers ----
     def score_host(self, batch: "HostBatchArrays", cfg: ScoreConfig, pool: list[torch.Tensor], fill: bool,
                    seed: int = 0, sigma: float = 2.0, stream=None, train: bool = False, n_global: float = 0.0,
-                   grad_pool: list[torch.Tensor] | None = None, grad_fn=None):
+                   grad_pool: list[torch.Tensor] | None = None, grad_fn=None, ref_fn=None):
         """Whole step through prorl_score_host. train=True runs K7 per micro-batch (loss partials + dL/dlogits,
         in place or into grad_pool); grad_fn(row0, n, grad_ptr, row_stride) sees each micro-batch's gradient."""
         if grad_pool is not None and len(grad_pool) != len(pool):
@@ -280,10 +280,22 @@ class Scorer:
                 except Exception:  # noqa: BLE001 — reported as a C status
                     return -3
             cb = N.GRAD_FN(_cb)
+        rcb, keep = None, []
+        if ref_fn is not None:
+            def _rcb(user, row0, n, rows, seq, cu, targets, out_ptr, strm):
+                try:
+                    r = ref_fn(row0, n, rows, seq, cu, targets)  # fp32 device tensor [n]
+                    keep[:] = [r]
+                    out_ptr[0] = r.data_ptr()
+                    return 0
+                except Exception:  # noqa: BLE001 — reported as a C status
+                    return -3
+            rcb = N.REF_FN(_rcb)
         lp = N.LogitsPool(C.cast(bufs, C.c_void_p), len(pool), 1 if fill else 0, pool[0].stride(0), seed, sigma, 0,
                           None, None, None, None, 0, 0, 0, 1 if train else 0, 0, float(n_global),
                           C.cast(gbufs, C.c_void_p) if gbufs is not None else None,
-                          C.cast(cb, C.c_void_p) if cb is not None else None, None)
+                          C.cast(cb, C.c_void_p) if cb is not None else None, None,
+                          C.cast(rcb, C.c_void_p) if rcb is not None else None, None)
         out = np.zeros(N.N_PARTIALS, dtype=np.float64)
         tm = np.zeros(5, dtype=np.float32)
         sc = cfg.c()

@@ -43,7 +43,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(N.ScoreCfg) == 40
     assert N.TURN_DTYPE.itemsize == 24
     assert C.sizeof(N.HostBatch) == 88
-    assert C.sizeof(N.LogitsPool) == 128
+    assert C.sizeof(N.LogitsPool) == 144
 
 
 def test_shard_lpt_deterministic_and_balanced():

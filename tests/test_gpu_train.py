@@ -307,3 +307,44 @@ def test_score_grad_errors(scorer, cuda):
     # zero rows: a no-op that leaves the partials untouched
     part, *_ = scorer.score_grad(x[:0], t[:0], f[:0], f, t[:0], tr[:0], 10.0)
     assert float(part.abs().sum()) == 0.0
+
+
+def test_score_host_kl_reference_logprobs(scorer, cuda):
+    """The k3 KL term through the whole step: reference logprobs
+    come from provide_ref per micro-batch; forward and training mode equal the
+    per-kernel path with ref_lp on the same logits; kl_coef without a source is
+    rejected."""
+    from paper_2603_18815_b200 import synth
+    from paper_2603_18815_b200.hotpath import RolloutError, ScoreConfig
+    from tests.test_gpu_parity import device_pack
+    sh = synth.make_shard("c1", seed=6)
+    b = sh.batch
+    V, mb = 32000, 2048
+    lcfg = LossConfig(kl_coef=0.25)
+    cfg = ScoreConfig(vocab=V, dtype="fp32", microbatch_rows=mb, loss=lcfg)
+    n_mb = -(-sh.n_active // mb)
+    pool = [torch.empty((mb, V), dtype=torch.float32, device=cuda) for _ in range(n_mb)]
+    gpool = [torch.empty_like(p) for p in pool]
+    ref_all = torch.from_numpy((-0.05 - 2.5 * np.random.default_rng(4).random(sh.n_active)).astype(np.float32)).to(cuda)
+    ref_fn = lambda row0, n, rows, seq, cu, tg: ref_all[row0:row0 + n]  # noqa: E731
+    with pytest.raises(RolloutError) as e:
+        scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7)
+    assert e.value.code == "malformed_request"
+    fwd, _ = scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7, ref_fn=ref_fn)
+    trn, _ = scorer.score_host(b.pinned(), cfg, pool, fill=True, seed=7, ref_fn=ref_fn, train=True, grad_pool=gpool)
+    torch.cuda.synchronize()
+    pk = device_pack(scorer, b, V, sh.n_active, cuda)
+    adv, _ = scorer.grpo_adv(torch.from_numpy(b.reward).to(cuda), torch.from_numpy(b.usable).to(cuda),
+                             torch.from_numpy(b.group_off).to(cuda))
+    acc = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=cuda)
+    for j in range(n_mb):
+        r0, n = j * mb, min(mb, sh.n_active - j * mb)
+        sl = slice(r0, r0 + n)
+        p, _, _ = scorer.score_rows(pool[j][:n], pk["act_target"][sl], pk["act_old_lp"][sl], adv, pk["act_seq"][sl],
+                                    pk["act_turn"][sl], cfg=lcfg, ref_lp=ref_all[sl])
+        acc += p
+    ref = acc.cpu().numpy()
+    assert ref[N.P_KL_SUM] > 0
+    for got in (fwd, trn):
+        for i in (N.P_LOSS_SUM, N.P_KL_SUM, N.P_ENTROPY_SUM, N.P_LOGP_SUM):
+            assert abs(got[i] - ref[i]) <= 2e-5 * abs(ref[i]) + 1e-6, (i, got[i], ref[i])
