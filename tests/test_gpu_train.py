@@ -4,10 +4,12 @@ oracle, and vs the two-pass K2+K4 -> K5 path it replaces.
 
 Tolerances as the kernels it fuses: logp/entropy |g - o| <= 1e-5 max(|o|, 1e-3);
 partial sums <= 1e-5 of the sum's condition scale, counts exact except rows
-within 1e-5 of a clip bound; dL/dlogp 1e-5 relative; gradient elements one
-bf16 rounding (2^-8 relative) for bf16, 1e-5 relative for fp32. Rows whose
-clip decision is within 1e-5 of flipping (oracle `border`) are skipped for
-the gradient."""
+within 1e-5 of a clip bound; dL/dlogp 1e-5 relative (plus, with the KL term,
+its sensitivity to logp times logp's own tolerance: a clipped row's KL-only
+scale kl/N (1 - e^(ref - logp)) is a small difference when ref ~ logp);
+gradient elements one bf16 rounding (2^-8 relative) for bf16, 1e-5 relative for
+fp32, plus the row scale's tolerance. Rows whose clip decision is within 1e-5
+of flipping (oracle `border`) are skipped for the gradient."""
 import numpy as np
 import pytest
 import torch
@@ -40,28 +42,36 @@ def _case(scorer, cuda, V, n, dtype, stride=None, seed=0, n_seq=11):
 
 
 def _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, n_global, rows=None, cfg=None, ref=None,
-               inplace=False):
+               inplace=False, inv_temp=1.0):
     kl = cfg.kl_coef if cfg else 0.0
     rd = None if rows is None else dev(rows, cuda)
     part, lp, ent, g, dl = scorer.score_grad(x, dev(t, cuda), dev(old, cuda), dev(adv, cuda), dev(seq, cuda),
                                              dev(turn, cuda), n_global, rows=rd, cfg=cfg, vocab=V,
                                              grad=x if inplace else None, want_dlogp=True,
-                                             ref_lp=None if ref is None else dev(ref, cuda))
+                                             ref_lp=None if ref is None else dev(ref, cuda), inv_temp=inv_temp)
     torch.cuda.synchronize()
-    olp, oent = O.logprob_entropy(host, t, rows=rows, vocab=V)
+    olp, oent = O.logprob_entropy(host, t, rows=rows, vocab=V, inv_temp=inv_temp)
     assert_rows_close(lp.cpu().numpy(), olp, "logp")
     assert_rows_close(ent.cpu().numpy(), oent, "entropy")
     P, Q, nb = O.loss(olp, oent, old, adv.astype(np.float64), seq, turn, ref_lp=ref, kl_coef=kl)
     assert_partials_close(part.cpu().numpy(), P, Q, nb, "k7")
     og, odl, bd = O.logits_grad(host, t, old, adv.astype(np.float64), seq, n_global, rows=rows, vocab=V,
-                                ref_lp=ref, kl_coef=kl)
+                                ref_lp=ref, kl_coef=kl, inv_temp=inv_temp)
     ok = bd == 0
     assert ok.sum() > 0.9 * len(ok)
     d = dl.cpu().numpy().astype(np.float64)
-    assert np.all(np.abs(d[ok] - odl[ok]) <= 1e-5 * np.abs(odl[ok]) + 1e-12)
+    # dL/dlogp to 1e-5, plus the KL term's sensitivity to logp times logp's own
+    # tolerance (a KL-only row, ref ~ logp, is a small difference: its relative
+    # error is the logp error amplified)
+    tol_dl = 1e-5 * np.abs(odl) + 1e-12
+    if ref is not None:
+        tol_dl += kl / n_global * np.exp(ref.astype(np.float64) - olp) * 1e-5 * np.maximum(np.abs(olp), 1e-3)
+    assert np.all(np.abs(d[ok] - odl[ok]) <= tol_dl[ok])
     r = np.arange(len(t)) if rows is None else rows
     got = g.float().cpu().numpy()[r, :V].astype(np.float64)
-    tol = (2.0 ** -8 if dtype == "bf16" else 1e-5) * np.abs(og) + 1e-30
+    # one bf16 rounding (fp32: 1e-5) plus the row scale's own tolerance (dL/dlogp)
+    row_rel = (tol_dl / np.maximum(np.abs(odl), 1e-300))[:, None]
+    tol = ((2.0 ** -8 if dtype == "bf16" else 1e-5) + row_rel) * np.abs(og) + 1e-30
     bad = (np.abs(got - og) > tol) & ok[:, None]
     assert not bad.any(), (np.argwhere(bad)[:5], got[bad][:5], og[bad][:5])
     return part, lp, ent, g, dl
@@ -280,8 +290,13 @@ def test_score_grad_randomized_layouts(scorer, cuda, case):
         cfg = LossConfig(kl_coef=0.1)
         lp0, _ = scorer.logprob_entropy(x, dev(t, cuda), rows=None if rows is None else dev(rows, cuda), vocab=V)
         ref = (lp0.cpu().numpy() + rng.normal(0, 0.3, n)).astype(np.float32)
+    inv_temp = float(rng.choice([1.0, 1.0, 0.7, 1.6]))
+    if ref is not None and inv_temp != 1.0:  # reference logprobs near this temperature's logprobs
+        lp0, _ = scorer.logprob_entropy(x, dev(t, cuda), rows=None if rows is None else dev(rows, cuda), vocab=V,
+                                        inv_temp=inv_temp)
+        ref = (lp0.cpu().numpy() + rng.normal(0, 0.3, n)).astype(np.float32)
     _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, dtype, float(n * 3), rows=rows, cfg=cfg, ref=ref,
-               inplace=rows is None and rng.random() < 0.5)
+               inplace=rows is None and rng.random() < 0.5, inv_temp=inv_temp)
 
 
 def test_score_grad_errors(scorer, cuda):
