@@ -41,7 +41,7 @@ struct ScoreConfig {
   float kl_coef = 0.0f;          // k3 KL vs a reference policy (1e-4); C-ABI ref_lp path
   int vocab = 0;
   LogitsDtype dtype = LogitsDtype::BF16;
-  int microbatch_rows = 16384;   // active rows per logits micro-batch
+  int microbatch_rows = 16576;   // active rows per logits micro-batch (7 waves of 148 x 16 K2 warps)
 };
 
 struct TurnMetrics {

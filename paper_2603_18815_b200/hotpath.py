@@ -43,7 +43,7 @@ class ScoreConfig:
     inv_temperature: float = 1.0
     adv_eps: float = 1e-6
     ddof: int = 1
-    microbatch_rows: int = 16384
+    microbatch_rows: int = 16576  # 7 waves of the 148 x 16 K2 warps
     loss: LossConfig = None
 
     def c(self) -> N.ScoreCfg:
