@@ -391,9 +391,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # PRORL_BENCH_DIST_BACKEND=gloo: orchestration check with several ranks
+    # sharing fewer GPUs (the library's NCCL communicator then cannot form and
+    # the partials are reduced through torch.distributed); numbers from such a
+    # run are not scaling numbers.
+    backend = os.environ.get("PRORL_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
+    coll = "cpu" if backend == "gloo" else "cuda"  # device of the torch.distributed tensors
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     c = synth.CONFIGS[args.config]
     # weak scaling: the global batch grows with the GPU count (tasks x N, same
     # seed), groups are LPT-sharded so every rank scores ~one config-sized shard
@@ -403,7 +413,9 @@ def run_ours(args):
     host = shard.batch.pinned()
     cfg = ScoreConfig(vocab=c["vocab"], dtype=c["dtype"], microbatch_rows=args.microbatch)
     sc = Scorer(local)
-    if world > 1:
+    if world > 1 and backend != "nccl":
+        torch_allreduce = True  # ranks may share a GPU: no library communicator
+    elif world > 1:
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         try:
@@ -426,7 +438,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # totals over ranks (weak scaling: each rank scores its own groups)
-    n_local = torch.tensor([shard.n_active], dtype=torch.float64, device="cuda")
+    n_local = torch.tensor([shard.n_active], dtype=torch.float64, device=coll)
     per_rank = [shard.n_active]
     if world > 1:
         gathered = [torch.zeros_like(n_local) for _ in range(world)]
@@ -446,7 +458,7 @@ def run_ours(args):
     for _ in range(args.steps):
         partials, tm = sc.score_host(host, cfg, pool, fill=False, seed=2603)
         if torch_allreduce:
-            pt = torch.from_numpy(partials).cuda()
+            pt = torch.from_numpy(partials).to(coll)
             dist.all_reduce(pt)
             partials = pt.cpu().numpy()
         seg += tm
@@ -473,7 +485,7 @@ def run_ours(args):
     e2e_ms = ev0.elapsed_time(ev1)
     dev_ms = float(seg[1] + seg[2] + seg[3])  # pack+GRPO, score, all-reduce (inputs resident)
     score_ms = float(seg[2])
-    t = torch.tensor([e2e_ms, dev_ms, score_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e2e_ms, dev_ms, score_ms], dtype=torch.float64, device=coll)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms, dev_ms, score_ms = (float(x) for x in t.tolist())
