@@ -70,7 +70,7 @@ struct prorl_ctx {
   prorl::DevBuf h_turns, h_ids, h_lp, h_reward, h_usable, h_goff;
   prorl::DevBuf p_tokens, p_mask, p_turn, p_seq, p_pos, p_cu, p_oldlp;
   prorl::DevBuf a_row, a_target, a_oldlp, a_seq, a_turn, a_nact;
-  prorl::DevBuf adv, informative, partials, logp, entropy, h_rkey, row_keys, lm_part;
+  prorl::DevBuf adv, informative, partials, logp, entropy, h_rkey, row_keys, lm_part, lm_pace;
   void* nccl_comm = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0;
   cudaEvent_t ev[8] = {};

@@ -52,6 +52,13 @@ struct LmParams {
   float c;           // inv_temp * log2 e
   const int32_t* targets;
   float* part;       // [n_rows][n_chunks][6]: Mc, Mx, S, T, xy, has_y
+  // Pacing (pair kernel, single wave over the whole vocabulary): producers
+  // publish each vocab tile they have issued in pace[tile] and do not issue
+  // tile n before every active worker has issued tile n - pace_window, so all
+  // workers stream the same few W tiles through L2 (null: no pacing).
+  int32_t* pace;
+  int32_t pace_workers;
+  int32_t pace_window;
 };
 
 // Work units u = chunk * m_tiles + m (chunk-major: CTAs running at the same
@@ -419,6 +426,25 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
+// Pacing counters (global memory, one int per vocab tile).
+__device__ __forceinline__ void pace_post(int32_t* cnt) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
+}
+__device__ __forceinline__ void pace_wait(const int32_t* cnt, int32_t target) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+  if (v >= target) return;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    __nanosleep(256);
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    if (v >= target) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_lmhead2(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, const LmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -467,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t u = q0; u < n_units; u += nq) {
         const Unit w = unit_of(p, u);
         for (int n = w.t0; n < w.t1; ++n) {
+          if (p.pace && rank == 0 && n >= p.pace_window) pace_wait(p.pace + (n - p.pace_window), p.pace_workers);
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait_bounded(&empty[s], ph ^ 1);
             const uint32_t bar = lm_mapa(smem_u32(&full[s]), 0);
@@ -478,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ph ^= 1;
             }
           }
+          if (p.pace && rank == 0) pace_post(p.pace + n);
         }
       }
     }
@@ -579,6 +607,18 @@ __global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, i
   if (entropy) entropy[i] = l1q + kLn2 * (fmaf(r, q, -T * ir) / (1.f + q));
 }
 
+// K6 pacing window in vocab tiles (PRORL_K6_PACE, 0 = off). Default 4: the
+// pairs stay within 4 W tiles (5 MB) of each other, W streams from HBM ~twice
+// instead of ~7x (ncu 1.7-2.2 GB vs 6.2 GB per 16 384-row launch), and the
+// saved DRAM energy buys clock at the power cap (whole step 570 vs 587 ms).
+int lmhead_pacing() {
+  static int w = [] {
+    const char* e = std::getenv("PRORL_K6_PACE");
+    return e ? std::max(0, std::atoi(e)) : 4;
+  }();
+  return w;
+}
+
 // K6 launch mode: CTA pairs (cta_group::2) unless PRORL_K6_PAIR=0.
 bool lmhead_pair_mode() {
   static bool pair = [] {
@@ -674,6 +714,14 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
   PRORL_CUDA(ctx->lm_part.ensure(sizeof(float) * 6 * (size_t)n_rows * (size_t)p.n_chunks));
   p.part = ctx->lm_part.as<float>();
   const int64_t units = (int64_t)p.m_tiles * p.n_chunks;
+  p.pace = nullptr;
+  if (pair && p.n_chunks == 1 && units <= n_workers && lmhead_pacing() > 0) {
+    PRORL_CUDA(ctx->lm_pace.ensure(sizeof(int32_t) * (size_t)p.n_ntiles));
+    PRORL_CUDA(cudaMemsetAsync(ctx->lm_pace.p, 0, sizeof(int32_t) * (size_t)p.n_ntiles, st));
+    p.pace = ctx->lm_pace.as<int32_t>();
+    p.pace_workers = (int32_t)units;  // one unit per active pair, every pair walks every vocab tile
+    p.pace_window = lmhead_pacing();
+  }
   if (pair) {
     const size_t smem = (size_t)STAGES2 * STAGE2_BYTES + 1024 + 256;
     PRORL_CUDA(cudaFuncSetAttribute(k_lmhead2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
