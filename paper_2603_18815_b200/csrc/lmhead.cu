@@ -430,6 +430,9 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 __device__ __forceinline__ void pace_post(int32_t* cnt) {
   asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
 }
+// Pacing is a hint, never a dependency: a worker waits at most ~200 us for the
+// slowest one, so a launch whose pairs are not all co-resident (a GPU shared
+// with other kernels) still makes progress, just without the L2 sharing.
 __device__ __forceinline__ void pace_wait(const int32_t* cnt, int32_t target) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
@@ -441,7 +444,7 @@ __device__ __forceinline__ void pace_wait(const int32_t* cnt, int32_t target) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
     if (v >= target) return;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 4000000000ull) __trap();
+    if (t - t0 > 200000ull) return;
   }
 }
 
