@@ -49,8 +49,8 @@ namespace {
 
 using namespace rowmath;
 
-constexpr int kPiece = 16384;                // bytes per bulk copy (ring slot)
-constexpr int kRing = 12;                    // ring pieces: 192 KB
+constexpr int kRingBytes = 196608;           // shared-memory ring per CTA: 192 KB
+constexpr int kPiece = 16384;                // bytes per bulk copy (ring slot) with a producer warp
 constexpr int kMaxWarps = 32;                // consumer warps of any launch configuration
 
 struct TrainArgs {
@@ -193,7 +193,7 @@ struct RowGeo {
   int npc, nsub, head, tail;
 };
 
-template <int ES, int kUnit>
+template <int ES, int kUnit, int PB>
 __device__ __forceinline__ RowGeo row_geo(const TrainArgs& p, int64_t r) {
   RowGeo g;
   g.rp = p.logits + r * p.stride_bytes;
@@ -205,7 +205,7 @@ __device__ __forceinline__ RowGeo row_geo(const TrainArgs& p, int64_t r) {
   if (b < a) b = a;
   g.a = a;
   g.nb = (uint32_t)(b - a);
-  g.npc = (int)((g.nb + kPiece - 1) / kPiece);
+  g.npc = (int)((g.nb + PB - 1) / PB);
   g.nsub = (int)((g.nb + kUnit - 1) / kUnit);
   g.head = (int)((a - st) / ES);
   g.tail = (int)((en - b) / ES);
@@ -225,9 +225,18 @@ __device__ __forceinline__ int64_t edge_index(const RowGeo& g, int l) {
 // per piece). G row groups: group g (W / G consumer warps, kRing / G ring
 // pieces, producer warp W + g) takes every G-th row of the CTA, so one group's
 // barrier and pipeline bubbles overlap the other's work (G = 1: one group).
-template <typename T, int SUBV, int W, int UNIT, int G>
-__global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
+//
+// SELF: no producer warps — pieces are single units (PB = UNIT), every ring
+// slot belongs to one consumer warp, and that warp's lane 0 refills the slot it
+// has just released with the piece kRG positions later in the stream (the same
+// warp's next piece there), exactly like K2's per-warp ring; no cross-warp
+// mbarrier hand-off remains.
+template <typename T, int SUBV, int W, int UNIT, int G, bool SELF>
+__global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const TrainArgs p) {
   constexpr int ES = Elem<T>::kSize;
+  constexpr int PB = SELF ? UNIT : kPiece;   // bytes per ring slot / bulk copy
+  constexpr int kRing = kRingBytes / PB;     // ring slots per CTA
+  constexpr int kPiece = PB;
   constexpr int kWarps = W / G;      // consumer warps per group
   constexpr int kRG = kRing / G;     // ring pieces per group
   constexpr int kUnit = UNIT;
@@ -268,13 +277,13 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
   for (int t = threadIdx.x; t < G * (kNG + kBucketDoubles); t += blockDim.x) gsum_all[t] = 0.0;
   __syncthreads();
 
-  if (warp >= W) {
+  if (!SELF && warp >= W) {
     // ===== producer: pass A (HBM, keep in L2) then pass B (L2) of each row =====
     if (lane == 0 && grp < G) {
       const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       uint32_t pc = 0;
       for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x) {
-        const RowGeo g = row_geo<ES, kUnit>(p, p.rows ? (int64_t)p.rows[i] : i);
+        const RowGeo g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
         const int fh = max(0, g.npc - kRG);  // pieces [fh, npc) stay in the ring for pass B
         for (int pass = 0; pass < 2; ++pass) {
           for (int k = 0; k < (pass == 0 ? g.npc : fh); ++k, ++pc) {
@@ -299,8 +308,59 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
   const uint4 fill = make_uint4(Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord);
   uint32_t pcb = 0;  // ring piece counter at the start of the row
   uint32_t j = 0;    // rows done by this CTA
+  // SELF: lane 0's feeder walks the group's piece stream (pass A pieces of a
+  // row, then its re-streamed pass-B pieces, then the next row) to load piece
+  // q into slot q % kRG; q only grows.
+  struct Feeder {
+    int64_t i;
+    uint32_t pcb;
+    RowGeo g;
+    int fh;
+  } fd;
+  uint64_t pol_a = 0, pol_b = 0;
+  auto feed = [&](uint32_t q) {
+    while (fd.i < p.n_rows && q >= fd.pcb + (uint32_t)(fd.g.npc + fd.fh)) {
+      fd.pcb += (uint32_t)(fd.g.npc + fd.fh);
+      fd.i += (int64_t)G * gridDim.x;
+      if (fd.i < p.n_rows) {
+        fd.g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[fd.i] : fd.i);
+        fd.fh = max(0, fd.g.npc - kRG);
+      }
+    }
+    if (fd.i >= p.n_rows) return;
+    const int k = (int)(q - fd.pcb);
+    const bool pass_a = k < fd.g.npc;
+    const int kp = pass_a ? k : k - fd.g.npc;
+    const int sl = (int)(q % kRG);
+    const uint32_t bytes = min((uint32_t)kPiece, fd.g.nb - (uint32_t)kp * kPiece);
+    fence_proxy_async_smem();  // this warp's reads of the slot before the async-proxy refill
+    mbar_arrive_expect_tx(&full[sl], bytes);
+    tma_load_1d(ring + (size_t)sl * kPiece, reinterpret_cast<const void*>(fd.g.a + (uintptr_t)kp * kPiece), bytes,
+                &full[sl], pass_a ? pol_a : pol_b);
+  };
+  // the slot of piece pc has been read by the whole warp: hand it on
+  auto release = [&](int sl, uint32_t pc) {
+    __syncwarp();
+    if (lane != 0) return;
+    if constexpr (SELF) feed(pc + (uint32_t)kRG);
+    else mbar_arrive_cnt(&empty[sl], 1u);
+  };
+  if constexpr (SELF) {
+    if (lane == 0) {
+      pol_a = l2_policy_evict_last();
+      pol_b = l2_policy_evict_first();
+      fd.i = blockIdx.x + (int64_t)grp * gridDim.x;
+      fd.pcb = 0;
+      fd.fh = 0;
+      if (fd.i < p.n_rows) {
+        fd.g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[fd.i] : fd.i);
+        fd.fh = max(0, fd.g.npc - kRG);
+      }
+      for (uint32_t q = (uint32_t)wq; q < (uint32_t)kRG; q += kWarps) feed(q);
+    }
+  }
   for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x, ++j) {
-    const RowGeo g = row_geo<ES, kUnit>(p, p.rows ? (int64_t)p.rows[i] : i);
+    const RowGeo g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
     const int32_t y = p.targets[i];
     float xy = 0.f, old = 0.f, A = 0.f, ref = 0.f;
     if (lane == 0) {
@@ -345,10 +405,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
           v[jj] = qv < nvv ? sv[qv] : fill;
         }
       }
-      if (k < fh) {  // streamed piece: free the slot; held pieces are released by pass B
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
-      }
+      if (k < fh) release(s, pc);  // streamed piece: free the slot; held pieces are released by pass B
 #pragma unroll
       for (int g0 = 0; g0 < kNV; g0 += SUBV) {
         uint4 w[SUBV];
@@ -471,8 +528,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
         const int s = (int)(pc % kRG);
         if (!held) mbar_wait_t(&full[s], (pc / kRG) & 1);
         if (u >= g.nsub) {  // padding unit of the last piece
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+          release(s, pc);
           continue;
         }
         const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)s * kPiece + (size_t)kk * kUnit);
@@ -485,8 +541,7 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
           const uint32_t qv = lane + 32 * jj;
           v[jj] = qv < nvv ? sv[qv] : make_uint4(0, 0, 0, 0);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cnt(&empty[s], 1u);
+        release(s, pc);
 #pragma unroll
         for (int jj = 0; jj < kNV; ++jj) {
           const uint32_t qv = lane + 32 * jj;
@@ -531,16 +586,16 @@ __global__ void __launch_bounds__((W + G) * 32, 1) k_train(const TrainArgs p) {
   }
 }
 
+constexpr int kMaxSlots = kRingBytes / 4096;  // smallest piece: 4 KB
 constexpr size_t train_smem_bytes() {
-  return (size_t)kRing * kPiece + (size_t)(2 * kRing) * 8 + (size_t)(2 * kMaxWarps) * 16 +
+  return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * 16 +
          (size_t)2 * (kNG + kBucketDoubles) * 8;
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
-static_assert(((size_t)kRing * kPiece + (size_t)(2 * kRing) * 8) % 16 == 0, "float4 partials alignment");
 
 // Launch configurations (consumer warps x unit bytes); PRORL_K7_CONFIG selects.
 constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w24u2048", "w12u4096", "w24u4096", "w16u4096g2",
-                                     "w16u2048g2", "w8u4096"};
+                                     "w16u2048g2", "w8u4096", "w16u4096s", "w16u4096g2s"};
 constexpr int kK7Default = 0, kK7TwoGroups = 5;
 
 // Default: two row groups per CTA when two rows per SM still fit the L2
@@ -559,15 +614,15 @@ int k7_config(int64_t row_bytes) {
   return row_bytes <= 160 * 1024 ? kK7TwoGroups : kK7Default;
 }
 
-template <typename T, int W, int UNIT, int G = 1>
+template <typename T, int W, int UNIT, int G = 1, bool SELF = false>
 int run_train_cfg(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
   constexpr int SUBV_BF16 = UNIT / 512 >= 8 ? 8 : UNIT / 512;
-  auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT, G>;
+  auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT, G, SELF>;
   constexpr size_t smem = train_smem_bytes();
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)std::min<int64_t>((int64_t)n_sm, a.n_rows);
   *rows_used = grid;
-  kern<<<grid, (W + G) * 32, smem, st>>>(a);
+  kern<<<grid, (W + (SELF ? 0 : G)) * 32, smem, st>>>(a);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
 }
@@ -582,6 +637,8 @@ int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
     case 5: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, rows_used, st);
     case 6: return run_train_cfg<T, 16, 2048, 2>(a, n_sm, rows_used, st);
     case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, rows_used, st);
+    case 8: return run_train_cfg<T, 16, 4096, 1, true>(a, n_sm, rows_used, st);
+    case 9: return run_train_cfg<T, 16, 4096, 2, true>(a, n_sm, rows_used, st);
     default: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
   }
 }
