@@ -107,7 +107,16 @@ struct RowRing {
   // Wait for the next chunk; returns its slot (16-B vectors).
   __device__ __forceinline__ const uint4* wait() {
     const int s = consumed % STAGES;
-    mbar_wait(&bars[s], (consumed / STAGES) & 1);
+    // bounded: a protocol bug traps after ~4 s instead of hanging the GPU
+    if (!mbar_try_wait(&bars[s], (consumed / STAGES) & 1)) {
+      uint64_t t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (uint32_t k = 1; !mbar_try_wait(&bars[s], (consumed / STAGES) & 1); ++k)
+        if ((k & 255u) == 0) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 4000000000ull) __trap();
+        }
+    }
     return reinterpret_cast<const uint4*>(ring + (size_t)s * CHUNK);
   }
 
