@@ -18,7 +18,7 @@ BIN = ROOT / "build" / "test_scoring"
 
 @pytest.fixture(scope="module")
 def binary():
-    B.build()
+    assert B.LIB.exists(), "libprorl_hotpath.so missing (conftest builds it on first use)"
     BIN.parent.mkdir(parents=True, exist_ok=True)
     src = ROOT / "tests" / "cpp" / "test_scoring.cpp"
     if not BIN.exists() or BIN.stat().st_mtime < max(src.stat().st_mtime, B.LIB.stat().st_mtime):
@@ -75,7 +75,7 @@ def test_cpp_score_responses_tool_vs_oracle(tmp_path):
     """tools/score_responses: wire JSON -> IngestedBatch -> DeviceScorer, all in C++."""
     from paper_2603_18815_b200 import synth
     from tests.wire import to_responses
-    B.build()
+    assert B.LIB.exists()
     exe = ROOT / "build" / "score_responses"
     src = ROOT / "tools" / "score_responses.cpp"
     if not exe.exists() or exe.stat().st_mtime < max(src.stat().st_mtime, B.LIB.stat().st_mtime):
