@@ -14,6 +14,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libprorl_hotpath.so"
+if os.environ.get("PRORL_HOTPATH_LIB"):  # A/B of an experimental build (scripts/build_variant.sh); never a fallback
+    LIB_PATH = Path(os.environ["PRORL_HOTPATH_LIB"]).resolve()
 
 PRORL_BF16, PRORL_FP32 = 0, 1
 ROLE_SYSTEM, ROLE_USER, ROLE_ASSISTANT, ROLE_TOOL = 0, 1, 2, 3
