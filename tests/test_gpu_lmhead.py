@@ -152,3 +152,20 @@ def test_score_host_lmhead_mode_matches_materialised_logits(scorer, cuda):
             assert abs(got[i] - ref[i]) <= 2, (i, got[i], ref[i])
         else:
             assert abs(got[i] - ref[i]) <= 1e-5 * max(abs(ref[i]), 1.0), (i, got[i], ref[i])
+
+
+@pytest.mark.parametrize("n,V", [(40000, 8192), (9000, 151936)])
+def test_lmhead_multi_wave_and_paced_schedules(scorer, cuda, n, V):
+    """Row counts that give several waves of CTA-pair units (no pacing) and a
+    single paced wave; sampled rows vs torch fp64."""
+    d = 256
+    g = torch.Generator(device=cuda).manual_seed(n)
+    H = torch.randn(n, d, device=cuda, generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, d, device=cuda, generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
+    t = torch.randint(0, V, (n,), device=cuda, dtype=torch.int32, generator=g)
+    lp, ent = scorer.lmhead_logprob(H, W, t)
+    idx = torch.cat([torch.arange(0, 300, device=cuda), torch.arange(n - 300, n, device=cuda),
+                     torch.randint(0, n, (400,), device=cuda, generator=g)])
+    rlp, rent = _ref(H[idx], W, t[idx], 1.0)
+    _check(lp[idx], rlp, "logp")
+    _check(ent[idx], rent, "entropy")
