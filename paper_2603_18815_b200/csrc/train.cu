@@ -50,7 +50,7 @@ namespace {
 using namespace rowmath;
 
 constexpr int kRingBytes = 196608;           // shared-memory ring per CTA: 192 KB
-constexpr int kPiece = 16384;                // bytes per bulk copy (ring slot) with a producer warp
+constexpr int kProducerPiece = 16384;        // bytes per bulk copy (ring slot) with producer warps
 constexpr int kMaxWarps = 32;                // consumer warps of any launch configuration
 
 struct TrainArgs {
@@ -234,7 +234,7 @@ __device__ __forceinline__ int64_t edge_index(const RowGeo& g, int l) {
 template <typename T, int SUBV, int W, int UNIT, int G, bool SELF>
 __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const TrainArgs p) {
   constexpr int ES = Elem<T>::kSize;
-  constexpr int PB = SELF ? UNIT : kPiece;   // bytes per ring slot / bulk copy
+  constexpr int PB = SELF ? UNIT : kProducerPiece;  // bytes per ring slot / bulk copy
   constexpr int kRing = kRingBytes / PB;     // ring slots per CTA
   constexpr int kPiece = PB;
   constexpr int kWarps = W / G;      // consumer warps per group
