@@ -179,27 +179,55 @@ def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
 def measure_train_whole_step(sc, host, cfg, pool, n_active, reps: int = 3) -> dict:
     """The whole per-GPU TRAINING step through the C-ABI (prorl_score_host,
     training mode): H2D, K1, K3, K7 per micro-batch (loss partials + bf16
-    dL/dlogits into a gradient pool), all-reduce, D2H; device time."""
+    dL/dlogits into a gradient pool), all-reduce, D2H; device time.
+
+    The logits pool holds 3 micro-batches, so the scoring bench re-scores
+    stale logits (targets not planted -> ratio ~ 0 -> every negative-advantage
+    row clips and has a zero gradient, whose pass B skips the exponentials).
+    Here every micro-batch is regenerated in the step (fill) so the gradient
+    density is the planted one (a few per cent of rows clip), and the
+    generator's time - the LM-head stand-in, outside the metric - is measured
+    on its own over the same micro-batch sizes and subtracted."""
     import numpy as np
     import torch
+    from paper_2603_18815_b200 import _native as N
     gpool = [torch.empty_like(b) for b in pool]  # grad_buffers[j % n_pool]: one per logits buffer
     for _ in range(2):
-        sc.score_host(host, cfg, pool, fill=False, seed=2603, train=True, grad_pool=gpool)
+        sc.score_host(host, cfg, pool, fill=True, seed=2603, train=True, grad_pool=gpool)
     torch.cuda.synchronize()
     tms = []
     for _ in range(reps):
-        _, tm = sc.score_host(host, cfg, pool, fill=False, seed=2603, train=True, grad_pool=gpool)
+        part, tm = sc.score_host(host, cfg, pool, fill=True, seed=2603, train=True, grad_pool=gpool)
         tms.append(tm)
     torch.cuda.synchronize()
     seg = np.mean(np.array(tms), axis=0)
-    dev_ms = float(seg[1] + seg[2] + seg[3])
-    e2e_ms = float(seg.sum())
+    # generator alone over the same micro-batch sizes (planted targets, as in fill)
+    mb, V = cfg.microbatch_rows, pool[0].shape[1]
+    sizes = [min(mb, n_active - r) for r in range(0, n_active, mb)]
+    tg = torch.randint(0, V, (mb,), device="cuda", dtype=torch.int32)
+    ol = torch.full((mb,), -1.3, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gen_ms = []
+    for _ in range(reps):
+        e0.record()
+        for j, n in enumerate(sizes):
+            sc.gen_logits(pool[j % len(pool)], n, j * mb, tg, ol, seed=2603)
+        e1.record()
+        torch.cuda.synchronize()
+        gen_ms.append(e0.elapsed_time(e1))
+    gen = float(np.median(gen_ms))
+    score = float(seg[2]) - gen
+    dev_ms = float(seg[1] + seg[3]) + score
+    e2e_ms = float(seg.sum()) - gen
+    na = float(part[N.P_N_ACTIVE])
     del gpool
     torch.cuda.empty_cache()
     return {"path": "prorl_score_host training mode (K1, K3, K7 per micro-batch: loss + bf16 dL/dlogits, all-reduce)",
-            "ms_per_step_device": dev_ms, "ms_per_step_e2e": e2e_ms, "score_ms": float(seg[2]),
+            "logits": "regenerated per micro-batch (planted targets); generator time measured alone and subtracted",
+            "generator_ms": gen, "ms_per_step_device": dev_ms, "ms_per_step_e2e": e2e_ms, "score_ms": score,
+            "clipped_rows_frac": float(part[N.P_CLIP_LO] + part[N.P_CLIP_HI]) / max(na, 1.0),
             "masked_tokens_per_s": n_active / (dev_ms / 1e3), "e2e_masked_tokens_per_s": n_active / (e2e_ms / 1e3),
-            "hbm_gbs_k7": n_active * (2 * (2 if cfg.dtype == "bf16" else 4) * cfg.vocab + 30) / (float(seg[2]) / 1e3) / 1e9}
+            "hbm_gbs_k7": n_active * (2 * (2 if cfg.dtype == "bf16" else 4) * cfg.vocab + 30) / (score / 1e3) / 1e9}
 
 
 def measure_train_step(sc, pool, c, args, reps: int = 10) -> dict:
@@ -435,6 +463,12 @@ def run_ours(args):
     # warm-up: the first call fills the pool with generated logits (LM-head stand-in)
     for w in range(max(args.warmup, 1)):
         partials, tm = sc.score_host(host, cfg, pool, fill=(w == 0), seed=2603)
+        if w == 0:  # the step whose logits match its targets (reported as "result")
+            fill_partials = partials.copy()
+            if torch_allreduce:
+                pt = torch.from_numpy(fill_partials).to(coll)
+                dist.all_reduce(pt)
+                fill_partials = pt.cpu().numpy()
     torch.cuda.synchronize()
 
     # totals over ranks (weak scaling: each rank scores its own groups)
@@ -508,7 +542,7 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        res = finalize(partials)
+        res = finalize(fill_partials)
         cpu = None
         ingest = None
         if world == 1 and not args.no_backward:
@@ -543,7 +577,8 @@ def run_ours(args):
             "segments_ms_per_step": {"h2d": seg[0] / K, "pack_grpo": seg[1] / K, "score": seg[2] / K,
                                      "allreduce": seg[3] / K, "d2h": seg[4] / K},
             "clocks": clk,
-            "result": {"loss": res["loss"], "entropy": res["entropy"], "clip_lo_frac": res["clip_lo_frac"],
+            "result": {"of": "the fill warm-up step (timed steps re-score the pooled logits; same cost)",
+                       "loss": res["loss"], "entropy": res["entropy"], "clip_lo_frac": res["clip_lo_frac"],
                        "clip_hi_frac": res["clip_hi_frac"], "n_active": res["n_active"]},
             "cpu_baseline": cpu,
             "backward": backward,

@@ -222,7 +222,7 @@ void oracle_gen_logits(void* out, int dtype, int64_t row_stride, int32_t vocab, 
                        const int32_t* targets, const float* old_lp, uint64_t seed, float sigma) {
   const uint32_t s0 = prorl_seed_mix(seed);
   const float scale = (float)((double)sigma * sqrt(3.0));
-  const float base = (float)(log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
+  const float base = prorl_plant_base(vocab, sigma);
   for (int64_t i = 0; i < n_rows; ++i) {
     const uint64_t key = (uint64_t)(row_key0 + i);
     for (int32_t c = 0; c < vocab; ++c) {

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "prorl_synth.h"
 
 namespace prorl {
 
@@ -336,7 +337,7 @@ int prorl_gen_logits(prorl_ctx* c, void* logits, int dtype, int64_t row_stride, 
   if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_gen_logits: null ctx");
   PRORL_CUDA(cudaSetDevice(c->device));
   const float scale = (float)((double)sigma * std::sqrt(3.0));
-  const float base = (float)(std::log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
+  const float base = prorl_plant_base(vocab, sigma);
   return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, row_key0, nullptr, targets, old_lp, seed, scale,
                            base, c->n_sm, S(stream));
 }
@@ -347,7 +348,7 @@ int prorl_gen_logits_keyed(prorl_ctx* c, void* logits, int dtype, int64_t row_st
   if (!c || !row_keys) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_gen_logits_keyed: null ctx/row_keys");
   PRORL_CUDA(cudaSetDevice(c->device));
   const float scale = (float)((double)sigma * std::sqrt(3.0));
-  const float base = (float)(std::log((double)vocab) + 0.5 * (double)sigma * (double)sigma);
+  const float base = prorl_plant_base(vocab, sigma);
   return launch_gen_logits(logits, dtype, row_stride, vocab, n_rows, 0, row_keys, targets, old_lp, seed, scale, base,
                            c->n_sm, S(stream));
 }
