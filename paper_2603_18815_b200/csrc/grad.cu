@@ -104,6 +104,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
     for (int64_t ch = 0; ch < nchunks; ++ch) {
       const uint32_t nvec = (uint32_t)(min((uintptr_t)CHUNK, b - (a + (uintptr_t)ch * CHUNK)) >> 4);
       const uint4* sv = rr.wait();
+      uint4* dst = reinterpret_cast<uint4*>(a + (uintptr_t)ch * CHUNK + (uintptr_t)goff);
+      if (!zero && nvec == (uint32_t)(CHUNK / 16)) {
+        // full chunk: load -> exps -> store per vector (the compiler barrier
+        // keeps the stores spread through the chunk instead of bunched)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const uint4 vj = sv[lane + 32 * j];
+          __stcs(dst + lane + 32 * j, GElem<T>::vec(vj, c2, nl2, s2));
+          asm volatile("" ::: "memory");
+        }
+        rr.release(lane);
+        continue;
+      }
       uint4 v[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
@@ -111,7 +124,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
         v[j] = q < nvec ? sv[q] : make_uint4(0, 0, 0, 0);
       }
       rr.release(lane);
-      uint4* dst = reinterpret_cast<uint4*>(a + (uintptr_t)ch * CHUNK + (uintptr_t)goff);
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         const uint32_t q = lane + 32 * j;

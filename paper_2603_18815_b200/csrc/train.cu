@@ -536,6 +536,29 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
         const int32_t tq = y_in ? yvec - u * (kUnit / 16) : -1;  // target vector inside this unit
         uint4* dst = reinterpret_cast<uint4*>(g.a + (uintptr_t)u * kUnit + (uintptr_t)p.goff);
         uint4 v[kNV];
+        if (nvv == (uint32_t)(kUnit / 16)) {
+          // full unit: no per-vector predicates; the target element (at most
+          // one per row) is re-stored by the lane that wrote its vector, after
+          // that vector (same thread, same address: program order)
+          if (zero) {
+            release(s, pc);
+#pragma unroll
+            for (int jj = 0; jj < kNV; ++jj) __stcs(dst + lane + 32 * jj, make_uint4(0, 0, 0, 0));
+          } else {
+            // load -> exps -> store per vector (the compiler barrier keeps the
+            // stores spread through the unit instead of bunched at its end)
+#pragma unroll
+            for (int jj = 0; jj < kNV; ++jj) {
+              const uint4 vj = sv[lane + 32 * jj];
+              __stcs(dst + lane + 32 * jj, GElem<T>::vec(vj, c2, nl2, s2));
+              asm volatile("" ::: "memory");
+            }
+            release(s, pc);
+            if ((uint32_t)tq < (uint32_t)(kUnit / 16) && lane == (tq & 31))
+              GElem<T>::store(reinterpret_cast<uint8_t*>(dst + tq), ye, gy);
+          }
+          continue;
+        }
 #pragma unroll
         for (int jj = 0; jj < kNV; ++jj) {
           const uint32_t qv = lane + 32 * jj;
