@@ -210,3 +210,19 @@ def test_oracle_grpo_and_loss_hand_computed():
     want = [-1.0, float(lo), -float(hi), 2.0]
     np.testing.assert_allclose(P[0], sum(want), rtol=1e-12)
     assert P[5] == 1 and P[6] == 1          # clip_lo (r<0.8, A<0), clip_hi (r>1.28, A>0)
+
+
+def test_synthetic_plant_is_unbiased():
+    """include/prorl_synth.h: the planted target gives logp = old_lp + U(-0.25, 0.25)
+    (noise log-mean of four uniforms + the target's own share of the partition
+    function), checked against the oracle's fp64 logprob over the generated rows."""
+    rng = np.random.default_rng(5)
+    for V, sigma in [(151936, 2.0), (32000, 1.0)]:
+        n = 96
+        t = rng.integers(0, V, n).astype(np.int32)
+        old = (-0.1 - 3.0 * rng.random(n)).astype(np.float32)
+        x = O.gen_logits(n, V, 0, t, old, seed=17, sigma=sigma, dtype="f32")
+        lp, _ = O.logprob_entropy(x, t)
+        d = lp - old
+        assert abs(d.mean()) < 0.05, (V, d.mean())
+        assert d.min() > -0.27 and d.max() < 0.27, (V, d.min(), d.max())
