@@ -293,7 +293,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
             fence_proxy_async_smem();  // the consumers' generic reads of this slot before the async-proxy refill
             mbar_arrive_expect_tx(&full[s], bytes);
             tma_load_1d(ring + (size_t)s * kPiece, reinterpret_cast<const void*>(g.a + (uintptr_t)k * kPiece), bytes,
-                        &full[s], pass == 0 ? pol_a : pol_b);
+                        &full[s], pass == 0 && k < fh ? pol_a : pol_b);
           }
         }
       }
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     fence_proxy_async_smem();  // this warp's reads of the slot before the async-proxy refill
     mbar_arrive_expect_tx(&full[sl], bytes);
     tma_load_1d(ring + (size_t)sl * kPiece, reinterpret_cast<const void*>(fd.g.a + (uintptr_t)kp * kPiece), bytes,
-                &full[sl], pass_a ? pol_a : pol_b);
+                &full[sl], pass_a && kp < fd.fh ? pol_a : pol_b);
   };
   // the slot of piece pc has been read by the whole warp: hand it on
   auto release = [&](int sl, uint32_t pc) {

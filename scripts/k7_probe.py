@@ -15,16 +15,19 @@ ap.add_argument("--rows", type=int, default=16576)
 ap.add_argument("--vocab", type=int, default=151936)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--fp32", action="store_true")
+ap.add_argument("--bufs", type=int, default=1, help="rotate over this many logits buffers (no L2 carry-over)")
 a = ap.parse_args()
 sc = Scorer(0)
 n, V = a.rows, a.vocab
 dt = torch.float32 if a.fp32 else torch.bfloat16
-x = torch.empty((n, V), dtype=dt, device="cuda")
+xs = [torch.empty((n, V), dtype=dt, device="cuda") for _ in range(a.bufs)]
+x = xs[0]
 gout = torch.empty_like(x)
 g = torch.Generator(device="cuda").manual_seed(7)
 t = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
 old = -0.05 - 2.9 * torch.rand(n, device="cuda", generator=g)
-sc.gen_logits(x, n, 0, t, old, seed=3, sigma=2.0)
+for xb in xs:
+    sc.gen_logits(xb, n, 0, t, old, seed=3, sigma=2.0)
 adv = torch.randn(64, device="cuda", generator=g)
 seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
 turn = torch.randint(0, 30, (n,), device="cuda", dtype=torch.int16, generator=g)
@@ -43,7 +46,15 @@ def timed(fn):
     return e0.elapsed_time(e1) / a.reps
 
 
-ms7 = timed(lambda: sc.score_grad(x, t, old, adv, seq, turn, float(n), grad=gout, want_rows=False))
+it = [0]
+
+
+def nxt():
+    it[0] += 1
+    return xs[it[0] % len(xs)]
+
+
+ms7 = timed(lambda: sc.score_grad(nxt(), t, old, adv, seq, turn, float(n), grad=gout, want_rows=False))
 ms2 = timed(lambda: sc.score_rows(x, t, old, adv, seq, turn))
 ms5 = timed(lambda: sc.logits_grad(x, t, old, old, adv, seq, float(n), grad=gout))
 bpr = 2 * V * x.element_size() + 30
