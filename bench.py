@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the global batch grows with N (default); strong: one config-sized batch split N ways")
     return ap.parse_args()
 
 
@@ -395,7 +397,7 @@ def run_reference(args):
     value = per_step * len(times) / sum(times)
     line = {"metric": "masked tokens/sec scored (logprob+GRPO loss)", "value": value, "unit": "masked tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic", "impl": "reference",
             "config": {"workload": c["desc"], "config_id": args.config, "active_rows_per_step": per_step,
                        "parallelism": "cpu threads"},
@@ -434,9 +436,10 @@ def run_ours(args):
             dist.init_process_group(backend)
     c = synth.CONFIGS[args.config]
     # weak scaling: the global batch grows with the GPU count (tasks x N, same
-    # seed), groups are LPT-sharded so every rank scores ~one config-sized shard
+    # seed), groups are LPT-sharded so every rank scores ~one config-sized shard;
+    # strong scaling: the config's batch itself is LPT-sharded over the ranks
     gcfg = dict(c)
-    gcfg["tasks"] = c["tasks"] * world
+    gcfg["tasks"] = c["tasks"] * (world if args.scaling == "weak" else 1)
     shard = synth.make_shard(gcfg, rank=rank, world=world, seed=2603 + c["index"])
     host = shard.batch.pinned()
     cfg = ScoreConfig(vocab=c["vocab"], dtype=c["dtype"], microbatch_rows=args.microbatch)
@@ -559,7 +562,7 @@ def run_ours(args):
         line = {
             "metric": "masked tokens/sec scored (logprob+GRPO loss)",
             "value": value, "unit": "masked tokens/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": c["dtype"], "data": "synthetic",
             "config": {"workload": c["desc"], "config_id": args.config, "parallelism": f"group-sharded dp{world}",
                        "tasks_global": gcfg["tasks"], "lpt_imbalance_max_over_mean": lpt_imbalance,
