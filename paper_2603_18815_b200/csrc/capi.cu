@@ -77,6 +77,16 @@ static int nccl_fail(ncclResult_t r, const char* what) {
     if (r_ != ncclSuccess) return ::prorl::nccl_fail(r_, #call); \
   } while (0)
 
+// PRORL_PDL=0 turns programmatic dependent launch between micro-batch
+// launches off (A/B); on by default.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PRORL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 #define PRORL_TRY(call)            \
   do {                             \
     int s_ = (call);               \
@@ -607,9 +617,12 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
       }
       continue;
     }
+    // back-to-back scoring launches (resident pool: no callback or generator
+    // work between them) overlap through programmatic dependent launch
+    const bool pdl = j > 0 && pdl_enabled() && !pool->provide && !pool->fill && !ref_lp;
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
                            pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp, n,
-                           cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st));
+                           cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st, pdl));
   }
   if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
   k_fold_errors<<<1, 1, 0, st>>>(c->d_err, partials);

@@ -31,6 +31,33 @@ int cuda_fail(cudaError_t e, const char* what);
     if (e_ != cudaSuccess) return ::prorl::cuda_fail(e_, #call); \
   } while (0)
 
+// Programmatic dependent launch between consecutive streaming launches of one
+// step (K2 / K7 micro-batches with no other work between them on the stream):
+// a kernel calls pdl_allow_next() at entry so the next launch's CTAs may take
+// SMs as its own CTAs exit (hiding the launch gap and the straggler tail), and
+// pdl_wait() before it touches anything the previous launch wrote (the slab
+// rows). Both are no-ops for a normally launched kernel.
+__device__ __forceinline__ void pdl_allow_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch `kern` (grid x block, dynamic smem) on `st`, with the programmatic
+// stream-serialization attribute when `pdl` is set.
+template <typename Kern, typename... Args>
+int launch_maybe_pdl(Kern kern, int grid, int block, size_t smem, bool pdl, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  PRORL_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+  return PRORL_OK;
+}
+
 // Growable device scratch owned by a ctx.
 struct DevBuf {
   void* p = nullptr;
@@ -92,7 +119,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
                  const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
                  const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                  float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
-                 bool accumulate, int* rows_used, cudaStream_t st);
+                 bool accumulate, int* rows_used, cudaStream_t st, bool pdl = false);
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp,
                 const float* adv, const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp,
                 int64_t n_rows, const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used,

@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
   constexpr int NV = CHUNK / 512;  // 16-B vectors per lane per chunk
   constexpr int ES = Elem<T>::kSize;
   extern __shared__ __align__(128) uint8_t smem[];
+  // the next scoring launch of the step (programmatic dependent launch) may
+  // take SMs as this grid's CTAs finish; it waits for this grid only before
+  // its slab update (pdl_allow_next / pdl_wait, common.cuh)
+  pdl_allow_next();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* ring = smem + (size_t)warp * STAGES * CHUNK;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CHUNK) + warp * STAGES;
@@ -254,6 +258,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
       for (int k = 0; k < kNG; ++k) g_w[warp * kNG + k] = g[k];
     }
     __syncthreads();
+    pdl_wait();  // the previous scoring launch's slab rows are complete and visible
     merge_block_partials<WARPS>(g_w, bk_w, p.slab, p.accumulate);
   }
 }
@@ -353,30 +358,28 @@ int active_config() {
 }
 
 template <typename T, int W, int ST, int CH, int SUBV_BF16, bool FUSED>
-int run_score_cfg(const ScoreArgs& a, int grid, cudaStream_t st) {
+int run_score_cfg(const ScoreArgs& a, int grid, bool pdl, cudaStream_t st) {
   constexpr int SUBV = sizeof(T) == 2 ? SUBV_BF16 : 4;
   auto kern = k_score<T, W, ST, CH, SUBV, FUSED>;
   constexpr size_t smem = score_smem_bytes<W, ST, CH, FUSED>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, W * 32, smem, st>>>(a);
-  PRORL_CUDA(cudaGetLastError());
-  return PRORL_OK;
+  return launch_maybe_pdl(kern, grid, W * 32, smem, pdl, st, a);
 }
 
 template <typename T, bool FUSED>
-int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* rows_used, cudaStream_t st) {
+int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* rows_used, bool pdl, cudaStream_t st) {
   const K2Config& k = kConfigs[active_config()];
   int grid = (int)std::min<int64_t>((int64_t)n_sm, (n_rows + k.warps - 1) / k.warps);
   if (FUSED && grid > slab_rows) grid = slab_rows;
   if (rows_used) *rows_used = grid;
   switch (active_config()) {
-    case 0: return run_score_cfg<T, 16, 2, 4096, 2, FUSED>(a, grid, st);
-    case 1: return run_score_cfg<T, 16, 2, 4096, 4, FUSED>(a, grid, st);
-    case 2: return run_score_cfg<T, 12, 3, 4096, 2, FUSED>(a, grid, st);
-    case 3: return run_score_cfg<T, 8, 5, 4096, 2, FUSED>(a, grid, st);
-    case 4: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, st);
-    default: return run_score_cfg<T, 16, 2, 4096, 8, FUSED>(a, grid, st);
+    case 0: return run_score_cfg<T, 16, 2, 4096, 2, FUSED>(a, grid, pdl, st);
+    case 1: return run_score_cfg<T, 16, 2, 4096, 4, FUSED>(a, grid, pdl, st);
+    case 2: return run_score_cfg<T, 12, 3, 4096, 2, FUSED>(a, grid, pdl, st);
+    case 3: return run_score_cfg<T, 8, 5, 4096, 2, FUSED>(a, grid, pdl, st);
+    case 4: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, pdl, st);
+    default: return run_score_cfg<T, 16, 2, 4096, 8, FUSED>(a, grid, pdl, st);
   }
 }
 
@@ -391,7 +394,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
                  const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
                  const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                  float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
-                 bool accumulate, int* rows_used, cudaStream_t st) {
+                 bool accumulate, int* rows_used, cudaStream_t st, bool pdl) {
   if (rows_used) *rows_used = 0;
   if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "score: unknown logits dtype");
   if (vocab <= 0 || row_stride < vocab) return fail(PRORL_E_SHAPE, "score: need vocab > 0 and row_stride >= vocab");
@@ -430,10 +433,10 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
     a.kl_coef = cfg->kl_coef;
   }
   if (dtype == PRORL_BF16)
-    return cfg ? run_score<__nv_bfloat16, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st)
-               : run_score<__nv_bfloat16, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st);
-  return cfg ? run_score<float, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st)
-             : run_score<float, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, st);
+    return cfg ? run_score<__nv_bfloat16, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, pdl, st)
+               : run_score<__nv_bfloat16, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, pdl, st);
+  return cfg ? run_score<float, true>(a, ctx->n_sm, n_rows, slab_rows, rows_used, pdl, st)
+             : run_score<float, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, pdl, st);
 }
 
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp, const float* adv,
