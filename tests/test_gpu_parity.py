@@ -369,6 +369,22 @@ def test_score_host_vs_oracle(scorer, cuda, config, kw):
     assert np.array_equal(got, again)  # deterministic run to run
 
 
+def test_score_host_resident_pool_back_to_back(scorer, cuda):
+    """A pool with one buffer per micro-batch: a fill step, then re-scoring the
+    resident logits (fill=False), whose micro-batch launches overlap through
+    programmatic dependent launch (capi.cu, PRORL_PDL) — bit-identical partials."""
+    sh = synth.make_shard("c1", seed=99)  # 6 144 active rows: 7 micro-batches
+    b = sh.batch.pinned()
+    cfg = _cfg("c1")
+    n_mb = (sh.n_active + cfg.microbatch_rows - 1) // cfg.microbatch_rows
+    assert n_mb >= 3
+    pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.float32, device=cuda) for _ in range(n_mb)]
+    filled, _ = scorer.score_host(b, cfg, pool, fill=True, seed=99)
+    for _ in range(3):
+        resident, _ = scorer.score_host(b, cfg, pool, fill=False, seed=99)
+        assert np.array_equal(filled, resident)
+
+
 def test_score_host_error_paths(scorer, cuda):
     sh = synth.make_shard("c1")
     b = sh.batch
