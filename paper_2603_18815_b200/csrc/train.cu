@@ -52,6 +52,7 @@ using namespace rowmath;
 constexpr int kRingBytes = 196608;           // shared-memory ring per CTA: 192 KB
 constexpr int kProducerPiece = 16384;        // bytes per bulk copy (ring slot) with producer warps
 constexpr int kMaxWarps = 32;                // consumer warps of any launch configuration
+constexpr int kMaxGroups = 4;                // row groups of any launch configuration
 
 struct TrainArgs {
   const uint8_t* logits;
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
   // round of its slots in order: a parity wait can never alias a round two
   // phases behind (pieces may complete out of order).
   constexpr int kPG = kWarps / kSplit;
-  static_assert(kNV % SUBV == 0 && kPiece % kUnit == 0 && W <= kMaxWarps && W % G == 0 && kRing % G == 0 &&
+  static_assert(kNV % SUBV == 0 && kPiece % kUnit == 0 && W <= kMaxWarps && G <= kMaxGroups && W % G == 0 && kRing % G == 0 &&
                     kWarps % kSplit == 0 && kRG % kPG == 0,
                 "launch configuration");
   extern __shared__ __align__(128) uint8_t smem[];
@@ -612,19 +613,24 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
 constexpr int kMaxSlots = kRingBytes / 4096;  // smallest piece: 4 KB
 constexpr size_t train_smem_bytes() {
   return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * 16 +
-         (size_t)2 * (kNG + kBucketDoubles) * 8;
+         (size_t)kMaxGroups * (kNG + kBucketDoubles) * 8;
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 
 // Launch configurations (consumer warps x unit bytes); PRORL_K7_CONFIG selects.
 constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w24u2048", "w12u4096", "w24u4096", "w16u4096g2",
-                                     "w16u2048g2", "w8u4096", "w16u4096s", "w16u4096g2s"};
-constexpr int kK7Default = 0, kK7TwoGroups = 5;
+                                     "w16u2048g2", "w8u4096", "w16u4096s", "w16u4096g2s", "w16u4096g4",
+                                     "w16u4096g4s"};
+constexpr int kK7Default = 0, kK7TwoGroups = 5, kK7FourGroups = 10;
 
-// Default: two row groups per CTA when two rows per SM still fit the L2
-// comfortably (row <= 160 KB: 296 rows in flight <= 48 MB) — measured 1.2-1.3x
-// at V = 32 000 / 65 536 — else one group (2x the rows in flight costs L2 hits:
-// -15 % at V = 151 936 bf16).
+// Default: row groups per CTA by row size. Short rows are dominated by the
+// per-row hand-offs (pass-A barrier, row results, the ring refilled only after
+// pass B), so more groups overlap more rows: four groups for rows <= 80 KB
+// (V = 32 000 bf16: 6.0 vs 5.1 TB/s with two), two while two rows per SM
+// still fit the L2 comfortably (row <= 160 KB: 296 rows in flight <= 48 MB;
+// 1.2-1.3x over one group at V = 32 000 fp32 / 65 536 bf16, where four
+// groups lose 16 %), else one group (more rows in flight cost L2 hits: -15 %
+// with two groups at V = 151 936 bf16).
 int k7_config(int64_t row_bytes) {
   static int forced = [] {
     const char* e = std::getenv("PRORL_K7_CONFIG");
@@ -634,6 +640,7 @@ int k7_config(int64_t row_bytes) {
     return -1;
   }();
   if (forced >= 0) return forced;
+  if (row_bytes <= 80 * 1024) return kK7FourGroups;
   return row_bytes <= 160 * 1024 ? kK7TwoGroups : kK7Default;
 }
 
@@ -662,6 +669,8 @@ int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
     case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, rows_used, st);
     case 8: return run_train_cfg<T, 16, 4096, 1, true>(a, n_sm, rows_used, st);
     case 9: return run_train_cfg<T, 16, 4096, 2, true>(a, n_sm, rows_used, st);
+    case 10: return run_train_cfg<T, 16, 4096, 4>(a, n_sm, rows_used, st);
+    case 11: return run_train_cfg<T, 16, 4096, 4, true>(a, n_sm, rows_used, st);
     default: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
   }
 }
