@@ -621,7 +621,7 @@ static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w24u2048", "w12u4096", "w24u4096", "w16u4096g2",
                                      "w16u2048g2", "w8u4096", "w16u4096s", "w16u4096g2s", "w16u4096g4",
                                      "w16u4096g4s"};
-constexpr int kK7Default = 0, kK7TwoGroups = 5, kK7FourGroups = 10;
+constexpr int kK7Default = 1, kK7TwoGroups = 5, kK7FourGroups = 10;
 
 // Default: row groups per CTA by row size. Short rows are dominated by the
 // per-row hand-offs (pass-A barrier, row results, the ring refilled only after
@@ -629,8 +629,9 @@ constexpr int kK7Default = 0, kK7TwoGroups = 5, kK7FourGroups = 10;
 // (V = 32 000 bf16: 6.0 vs 5.1 TB/s with two), two while two rows per SM
 // still fit the L2 comfortably (row <= 160 KB: 296 rows in flight <= 48 MB;
 // 1.2-1.3x over one group at V = 32 000 fp32 / 65 536 bf16, where four
-// groups lose 16 %), else one group (more rows in flight cost L2 hits: -15 %
-// with two groups at V = 151 936 bf16).
+// groups lose 16 %), else one group of 16 warps on 2 KB units (more rows in
+// flight cost L2 hits: -15 % with two groups at V = 151 936 bf16; 2 KB units
+// beat 4 KB by 0-2.5 % from V = 128 256 to 262 144).
 int k7_config(int64_t row_bytes) {
   static int forced = [] {
     const char* e = std::getenv("PRORL_K7_CONFIG");
