@@ -8,14 +8,15 @@
 // row from HBM after the forward has produced its lse. K7 moves 4V.
 //
 //   * One CTA per SM, persistent over rows. The CTA's consumer warps form G row
-//     groups (G = 2 for rows <= 160 KB, else 1); a group owns ONE row at a
-//     time, so the rows in flight (148 x G x 2V bytes: 45 MB at V = 151 936
-//     bf16) fit in the 126 MB L2 between the two passes over each row, and one
-//     group's barrier and pipeline bubbles overlap the other group's work.
+//     groups (G = 4 for rows <= 80 KB, 2 for <= 160 KB, else 1); a group owns
+//     ONE row at a time, so the rows in flight (148 x G x 2V bytes: 45 MB at
+//     V = 151 936 bf16) fit in the 126 MB L2 between the two passes over each
+//     row, and one group's barrier and pipeline bubbles overlap the others'.
 //   * Pass A (statistics): the group's producer warp streams the row from HBM
 //     into the group's shared-memory ring of 16 KB pieces (1-D TMA bulk
-//     copies, L2 evict_last). Piece P goes to a fixed set of kSplit warps, one
-//     4 KB unit each, so every warp sees every round of its ring slots in
+//     copies; L2 evict_last on the pieces pass B re-reads). Piece P goes to a
+//     fixed set of kSplit warps, one 2 or 4 KB unit each (config), so every
+//     warp sees every round of its ring slots in
 //     order (a parity wait never aliases a round two phases back; pieces can
 //     complete out of order). Warps run K2's online base-2 logsumexp
 //     (warp-uniform running max, top element kept out of the sums); the warp
