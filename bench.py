@@ -504,15 +504,19 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and not args.no_backward else None
+    # single-GPU kernel side measurements: N=1 only (at N>1 the whole-step ones
+    # would put extra all-reduces on every rank, and one rank failing there
+    # would leave its peers waiting in the collective)
+    extras = world == 1 and not args.no_backward
+    backward = measure_backward(sc, pool, c, args) if args.pool >= 2 and extras else None
     train_step = None
-    if args.pool >= 2 and not args.no_backward:
+    if args.pool >= 2 and extras:
         try:
             train_step = measure_train_step(sc, pool, c, args)
             train_step["whole_step"] = measure_train_whole_step(sc, host, cfg, pool, shard.n_active)
         except Exception as ex:
             train_step = {"error": repr(ex)}
-    lmhead = measure_lmhead(sc, c, args) if not args.no_backward and c["dtype"] == "bf16" else None
+    lmhead = measure_lmhead(sc, c, args) if extras and c["dtype"] == "bf16" else None
     lmhead_step = None
     if lmhead is not None:
         del pool  # free the 15 GB logits pool: this path never materialises logits
