@@ -158,7 +158,7 @@ def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
     targets = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
     logp, _ = sc.logprob_entropy(pool[0], targets)
     old = logp + 0.3 * (torch.rand(n, device="cuda", generator=g) - 0.5)
-    adv = torch.randn(64, device="cuda", generator=g)
+    adv = torch.randn(64, device="cuda", generator=g, dtype=torch.float64)
     seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
     for _ in range(2):
         sc.logits_grad(pool[0], targets, logp, old, adv, seq, float(n), grad=pool[1])
@@ -244,7 +244,7 @@ def measure_train_step(sc, pool, c, args, reps: int = 10) -> dict:
     targets = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
     logp, _ = sc.logprob_entropy(pool[0], targets)
     old = logp + 0.3 * (torch.rand(n, device="cuda", generator=g) - 0.5)
-    adv = torch.randn(64, device="cuda", generator=g)
+    adv = torch.randn(64, device="cuda", generator=g, dtype=torch.float64)
     seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
     turn = torch.randint(0, 30, (n,), device="cuda", dtype=torch.int16, generator=g)
     part = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device="cuda")

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define PRORL_ABI_VERSION 1
+#define PRORL_ABI_VERSION 2  /* 2: prorl_score_cfg.gate_tolerance; advantages fp64 */
 
 typedef enum prorl_status {
   PRORL_OK = 0,
@@ -130,6 +130,8 @@ typedef struct prorl_score_cfg {
   int32_t vocab;         /* V */
   int32_t dtype;         /* prorl_dtype of logits */
   int32_t microbatch_rows; /* active rows per logits micro-batch */
+  double gate_tolerance;   /* is_informative tolerance (harness.cpp:92-102; default 0 = exact).
+                            * K3 gates with it; host batches must be built with the same value */
 } prorl_score_cfg;
 
 /* ---- context / errors ----------------------------------------------------- */
@@ -154,13 +156,13 @@ int prorl_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns,
 
 /* ---- K3: GRPO advantages -------------------------------------------------- */
 /* reward: [n_rollouts] fp64, usable: [n_rollouts] (0 = FAILED), group_off:
- * [n_groups+1] int32 rollout offsets. adv [n_rollouts] fp32 (0 for
+ * [n_groups+1] int32 rollout offsets. adv [n_rollouts] fp64 (0 for
  * non-usable rollouts and non-informative groups), informative [n_groups].
  * partials (nullable): adds sum(adv) and N_rollouts (usable rollouts of
  * informative groups) into partials[8], partials[9]. */
 int prorl_grpo_adv(prorl_ctx* ctx, const double* reward, const uint8_t* usable,
                    const int32_t* group_off, int32_t n_groups, int32_t ddof, float eps,
-                   double tolerance, float* adv, uint8_t* informative, double* partials,
+                   double tolerance, double* adv, uint8_t* informative, double* partials,
                    void* stream);
 
 /* ---- K2: logprob + entropy over the vocabulary ------------------------------ */
@@ -178,7 +180,7 @@ int prorl_logprob_entropy(prorl_ctx* ctx, const void* logits, int dtype, int64_t
  * kl_coef * k3 to its loss, k3 = exp(ref - logp) - (ref - logp) - 1, and
  * sum(k3) to partials[PRORL_P_KL_SUM]. */
 int prorl_clipped_loss(prorl_ctx* ctx, const float* logp, const float* entropy,
-                       const float* old_lp, const float* adv, const int32_t* row_seq,
+                       const float* old_lp, const double* adv, const int32_t* row_seq,
                        const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                        const prorl_loss_cfg* cfg, double* partials_dev, void* stream);
 
@@ -186,7 +188,7 @@ int prorl_clipped_loss(prorl_ctx* ctx, const float* logp, const float* entropy,
  * logp/entropy outputs are optional (may be NULL). */
 int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride,
                      int32_t vocab, const int32_t* rows, const int32_t* targets,
-                     const float* old_lp, const float* adv, const int32_t* row_seq,
+                     const float* old_lp, const double* adv, const int32_t* row_seq,
                      const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float inv_temp,
                      const prorl_loss_cfg* cfg, float* logp, float* entropy,
                      double* partials_dev, void* stream);
@@ -202,7 +204,7 @@ int prorl_score_rows(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_
  * k3 KL term adds kl_coef * (1 - exp(ref - logp)) / n_global to g_i. */
 int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                       const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
-                      const float* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
+                      const double* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride,
                       float* dlogp, void* stream);
 
@@ -216,7 +218,7 @@ int prorl_logits_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row
  * Same layouts as prorl_logits_grad: grad_stride == row_stride, grad with
  * the logits' 16-B phase, grad may alias logits (in place). */
 int prorl_score_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
-                     const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                     const int32_t* rows, const int32_t* targets, const float* old_lp, const double* adv,
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                      float inv_temp, const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy,
                      double* partials_dev, void* grad, int64_t grad_stride, float* dlogp, void* stream);

@@ -1,12 +1,14 @@
-// rollout/trainer/harness.hpp — the trainer-side group types the scoring path
-// consumes, drop-in for the reference declarations
-// (proj/include/rollout/trainer/harness.hpp:35-84):
+// rollout/trainer/harness.hpp — STANDALONE re-declaration of the trainer-side
+// group types the scoring path consumes, for builds of this repo without the
+// reference tree (a reference build never sees include/standalone/). Same
+// members as the reference (proj/include/rollout/trainer/harness.hpp:35-84):
 //   RolloutOutcome, PromptGroup{completed_count, complete, usable_rewards},
 //   is_informative, IterationStats::informative (the hand-off point).
-// Additive change: RolloutOutcome gains an optional
-// trajectory slot, filled from the /process response's "trajectory" field that
-// the reference harness drops today (proj/src/trainer/harness.cpp:263-273).
-// The scheduling half of the reference harness (TrainerHarness) is out of scope.
+// RolloutOutcome is unchanged — the token trajectory travels beside it in the
+// façade's TrajectoryTable (include/rollout/trainer/scoring.hpp). The
+// reference defines the PromptGroup members and is_informative out of line in
+// proj/src/trainer/harness.cpp:71-102; here they are inline. The scheduling
+// half of the reference harness (TrainerHarness) is out of scope.
 #pragma once
 
 #include <algorithm>
@@ -17,7 +19,6 @@
 #include <json.hpp>
 
 #include "rollout/errors.hpp"
-#include "rollout/trajectory.hpp"
 
 namespace rollout::train {
 
@@ -28,9 +29,6 @@ struct RolloutOutcome {
   std::string status;   // DONE / FAILED / CANCELLED
   std::string address;  // backend that served it, when reported
   double wall_seconds = 0.0;
-  std::optional<TokenTrajectory> trajectory;  // additive: token-level trajectory
-
-  bool failed() const { return status == "FAILED"; }
 };
 
 struct PromptGroup {
@@ -51,7 +49,7 @@ struct PromptGroup {
     std::vector<double> r;
     r.reserve(outcomes.size());
     for (const auto& o : outcomes)
-      if (o && !o->failed()) r.push_back(o->reward);
+      if (o && o->status != "FAILED") r.push_back(o->reward);
     return r;
   }
 };

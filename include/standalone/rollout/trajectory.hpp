@@ -1,5 +1,8 @@
-// rollout/trajectory.hpp — token-level multi-turn trajectory, drop-in for the
-// reference type of the same name (proj/include/rollout/trajectory.hpp).
+// rollout/trajectory.hpp — STANDALONE re-declaration of the reference type of
+// the same name (proj/include/rollout/trajectory.hpp:11-103), for builds of
+// this repo without the reference tree. Same members, no extras: the façade
+// (include/rollout/trainer/scoring.hpp) compiles against either header. A
+// reference build never sees this directory (include/standalone/).
 //
 // Semantics preserved exactly, because the device packer (prorl_pack) is
 // defined in terms of them:
@@ -14,7 +17,6 @@
 
 #include <algorithm>
 #include <cstddef>
-#include <numeric>
 #include <string>
 #include <vector>
 
@@ -37,9 +39,6 @@ struct Turn {
   TokenIds output_ids;         // assistant turns
   std::vector<double> logprobs;  // aligned with output_ids (behaviour policy)
   std::string text;            // display only, never re-tokenized
-
-  // The ids this turn contributes to the flattened stream.
-  const TokenIds& tokens() const { return role == Role::ASSISTANT ? output_ids : input_ids; }
 };
 
 inline Turn make_user_turn(TokenIds ids, std::string text = {}) {
@@ -75,12 +74,6 @@ class TokenTrajectory {
   std::size_t size() const { return turns_.size(); }
   bool empty() const { return turns_.empty(); }
 
-  // Number of tokens flatten() yields.
-  std::size_t token_count() const {
-    return std::accumulate(turns_.begin(), turns_.end(), std::size_t{0},
-                           [](std::size_t n, const Turn& t) { return n + t.tokens().size(); });
-  }
-
   TokenIds flatten() const { return flatten_range(0, turns_.size()); }
 
   // Turns [begin, end), end clamped to size().
@@ -88,7 +81,8 @@ class TokenTrajectory {
     TokenIds out;
     const std::size_t stop = std::min(end, turns_.size());
     for (std::size_t i = begin; i < stop; ++i) {
-      const TokenIds& ids = turns_[i].tokens();
+      const Turn& t = turns_[i];
+      const TokenIds& ids = t.role == Role::ASSISTANT ? t.output_ids : t.input_ids;
       out.insert(out.end(), ids.begin(), ids.end());
     }
     return out;

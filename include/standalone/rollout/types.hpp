@@ -1,5 +1,6 @@
-// rollout/types.hpp — the token and sampling types the scoring path consumes,
-// with the reference's names and meaning (proj/include/rollout/types.hpp:12-13
+// rollout/types.hpp — STANDALONE re-declaration (never seen by a reference
+// build) of the token and sampling types the scoring path consumes, with the
+// reference's names and meaning (proj/include/rollout/types.hpp:12-13
 // TokenId = int64 on the wire; :58-71 SamplingParams, whose temperature is the
 // logit temperature of the logprob pass).
 #pragma once

@@ -432,7 +432,8 @@ int oracle_score_batch(const prorl_host_batch* hb, const prorl_score_cfg* cfg, u
   double* adv = malloc((size_t)(R > 0 ? R : 1) * sizeof(double));
   uint8_t* info = malloc((size_t)(hb->n_groups > 0 ? hb->n_groups : 1));
   double asum = 0.0, nr = 0.0;
-  if (st == 0) oracle_grpo(hb->reward, hb->usable, hb->group_off, hb->n_groups, cfg->ddof, (double)cfg->adv_eps, 0.0,
+  if (st == 0) oracle_grpo(hb->reward, hb->usable, hb->group_off, hb->n_groups, cfg->ddof, (double)cfg->adv_eps,
+                           cfg->gate_tolerance,
                            adv, info, &asum, &nr);
   double t1 = now_s();
   if (st == 0) {

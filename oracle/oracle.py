@@ -40,7 +40,7 @@ class LossCfg(C.Structure):  # layout of prorl_loss_cfg (include/prorl_hotpath.h
 
 class ScoreCfg(C.Structure):  # layout of prorl_score_cfg
     _fields_ = [("loss", LossCfg), ("inv_temperature", f32), ("adv_eps", f32), ("ddof", i32), ("vocab", i32),
-                ("dtype", i32), ("microbatch_rows", i32)]
+                ("dtype", i32), ("microbatch_rows", i32), ("gate_tolerance", f64)]
 
 
 class HostBatch(C.Structure):  # layout of prorl_host_batch
@@ -55,9 +55,9 @@ def host_batch(turns, ids, lp, reward, usable, group_off, rollout_key=None) -> H
 
 
 def score_cfg(vocab, dtype="bf16", inv_temperature=1.0, adv_eps=1e-6, ddof=1, eps_lo=0.2, eps_hi=0.28,
-              n_buckets=64, microbatch_rows=16384) -> ScoreCfg:
+              n_buckets=64, microbatch_rows=16384, gate_tolerance=0.0) -> ScoreCfg:
     return ScoreCfg(LossCfg(eps_lo, eps_hi, n_buckets, 0), inv_temperature, adv_eps, ddof, vocab,
-                    0 if dtype == "bf16" else 1, microbatch_rows)
+                    0 if dtype == "bf16" else 1, microbatch_rows, gate_tolerance)
 
 
 def _p(a):

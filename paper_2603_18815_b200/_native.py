@@ -51,7 +51,8 @@ class LossCfg(C.Structure):
 
 class ScoreCfg(C.Structure):
     _fields_ = [("loss", LossCfg), ("inv_temperature", C.c_float), ("adv_eps", C.c_float), ("ddof", C.c_int32),
-                ("vocab", C.c_int32), ("dtype", C.c_int32), ("microbatch_rows", C.c_int32)]
+                ("vocab", C.c_int32), ("dtype", C.c_int32), ("microbatch_rows", C.c_int32),
+                ("gate_tolerance", C.c_double)]
 
 
 class HostBatch(C.Structure):

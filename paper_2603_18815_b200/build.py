@@ -21,7 +21,7 @@ INCLUDE = ROOT / "include"
 BUILD = ROOT / "build" / "hotpath"
 LIB = PKG / "libprorl_hotpath.so"
 
-SOURCES = ["pack.cu", "grpo.cu", "score.cu", "grad.cu", "train.cu", "lmhead.cu", "synth.cu", "capi.cu", "workload.cpp", "scoring.cpp", "ingest.cpp"]
+SOURCES = ["pack.cu", "grpo.cu", "score.cu", "grad.cu", "train.cu", "lmhead.cu", "synth.cu", "capi.cu", "workload.cpp", "ingest.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]

@@ -126,7 +126,7 @@ using namespace prorl;
 static_assert(sizeof(prorl_turn_desc) == 24, "prorl_turn_desc layout");
 static_assert(sizeof(prorl_packed) == 13 * 8, "prorl_packed layout");
 static_assert(sizeof(prorl_loss_cfg) == 16, "prorl_loss_cfg layout");
-static_assert(sizeof(prorl_score_cfg) == 40, "prorl_score_cfg layout");
+static_assert(sizeof(prorl_score_cfg) == 48, "prorl_score_cfg layout");
 static_assert(sizeof(prorl_host_batch) == 88, "prorl_host_batch layout");
 static_assert(sizeof(prorl_logits_pool) == 144, "prorl_logits_pool layout");
 static_assert(sizeof(prorl_ingest_result) == 112, "prorl_ingest_result layout");
@@ -210,7 +210,7 @@ int prorl_pack(prorl_ctx* c, const prorl_turn_desc* turns, int64_t n_turns, cons
 }
 
 int prorl_grpo_adv(prorl_ctx* c, const double* reward, const uint8_t* usable, const int32_t* group_off,
-                   int32_t n_groups, int32_t ddof, float eps, double tolerance, float* adv, uint8_t* informative,
+                   int32_t n_groups, int32_t ddof, float eps, double tolerance, double* adv, uint8_t* informative,
                    double* partials, void* stream) {
   if (!c) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_grpo_adv: null ctx");
   PRORL_CUDA(cudaSetDevice(c->device));
@@ -227,7 +227,7 @@ int prorl_logprob_entropy(prorl_ctx* c, const void* logits, int dtype, int64_t r
                       n_rows, inv_temp, nullptr, logp, entropy, nullptr, 0, false, nullptr, S(stream));
 }
 
-int prorl_clipped_loss(prorl_ctx* c, const float* logp, const float* entropy, const float* old_lp, const float* adv,
+int prorl_clipped_loss(prorl_ctx* c, const float* logp, const float* entropy, const float* old_lp, const double* adv,
                        const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                        const prorl_loss_cfg* cfg, double* partials_dev, void* stream) {
   if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_clipped_loss: null ctx/cfg");
@@ -241,7 +241,7 @@ int prorl_clipped_loss(prorl_ctx* c, const float* logp, const float* entropy, co
 }
 
 int prorl_score_rows(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
-                     const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                     const int32_t* rows, const int32_t* targets, const float* old_lp, const double* adv,
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                      float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* partials_dev,
                      void* stream) {
@@ -257,7 +257,7 @@ int prorl_score_rows(prorl_ctx* c, const void* logits, int dtype, int64_t row_st
 
 int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
                       const int32_t* rows, const int32_t* targets, const float* logp, const float* old_lp,
-                      const float* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
+                      const double* adv, const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                       const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride, float* dlogp,
                       void* stream) {
   if (!c || !cfg) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_logits_grad: null ctx/cfg");
@@ -267,7 +267,7 @@ int prorl_logits_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_s
 }
 
 int prorl_score_grad(prorl_ctx* c, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
-                     const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                     const int32_t* rows, const int32_t* targets, const float* old_lp, const double* adv,
                      const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                      float inv_temp, const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy,
                      double* partials_dev, void* grad, int64_t grad_stride, float* dlogp, void* stream) {
@@ -441,6 +441,21 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: kl_coef != 0 needs provide_ref (reference logprobs)");
   if (train_mode && lmhead_mode)
     return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: training mode needs the logits path (no fused LM head)");
+  // the gradient is normalised by n_global while the reported loss is the
+  // all-reduced token mean: with several ranks only the caller knows the global count
+  if (train_mode && !(pool->n_global > 0.0) && c->nranks > 1)
+    return fail(PRORL_E_MALFORMED_REQUEST,
+                "prorl_score_host: training with more than one rank needs n_global (the global active-row count)");
+  // configuration, checked once before any device work (the launchers re-check their own arguments)
+  if (cfg->dtype != PRORL_BF16 && cfg->dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "prorl_score_host: unknown dtype");
+  if (cfg->vocab <= 0) return fail(PRORL_E_SHAPE, "prorl_score_host: vocab must be > 0");
+  if (!(cfg->inv_temperature > 0.f)) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: inv_temperature must be > 0");
+  if (cfg->loss.n_buckets < 1 || cfg->loss.n_buckets > PRORL_TURN_BUCKETS)
+    return fail(PRORL_E_SHAPE, "prorl_score_host: n_buckets out of [1, 64]");
+  if (cfg->ddof != 0 && cfg->ddof != 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: ddof must be 0 or 1");
+  if (!(cfg->gate_tolerance >= 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_score_host: gate_tolerance must be >= 0");
+  if (!lmhead_mode && !pool->provide && pool->row_stride < cfg->vocab)
+    return fail(PRORL_E_SHAPE, "prorl_score_host: pool row_stride < vocab");
   if (hb->n_groups < 0 || hb->n_rollouts < 0 || hb->n_turns < 0 || hb->n_tokens < 0)
     return fail(PRORL_E_SHAPE, "prorl_score_host: negative sizes");
   if ((hb->n_turns > 0 && !hb->turns) || (hb->n_tokens > 0 && (!hb->ids || !hb->lp)) ||
@@ -489,7 +504,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   PRORL_CUDA(c->a_seq.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(A, 1)));
   PRORL_CUDA(c->a_turn.ensure(sizeof(int16_t) * (size_t)std::max<int64_t>(A, 1)));
   PRORL_CUDA(c->a_nact.ensure(sizeof(int64_t)));
-  PRORL_CUDA(c->adv.ensure(sizeof(float) * (size_t)std::max(R, 1)));
+  PRORL_CUDA(c->adv.ensure(sizeof(double) * (size_t)std::max(R, 1)));
   PRORL_CUDA(c->h_rkey.ensure(sizeof(int64_t) * (size_t)std::max(R, 1)));
   PRORL_CUDA(c->row_keys.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(std::min<int64_t>(A, cfg->microbatch_rows), 1)));
   PRORL_CUDA(c->informative.ensure((size_t)std::max(G, 1)));
@@ -542,8 +557,13 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   PRORL_TRY(launch_pack(c, c->h_turns.as<prorl_turn_desc>(), hb->n_turns, c->h_ids.as<int64_t>(),
                         c->h_lp.as<double>(), N, R, cfg->vocab, &pk, st));
   PRORL_TRY(launch_grpo(c, c->h_reward.as<double>(), c->h_usable.as<uint8_t>(), c->h_goff.as<int32_t>(), G, cfg->ddof,
-                        cfg->adv_eps, 0.0, c->adv.as<float>(), c->informative.as<uint8_t>(), partials, st));
+                        cfg->adv_eps, cfg->gate_tolerance, c->adv.as<double>(), c->informative.as<uint8_t>(), partials,
+                        st));
   PRORL_CUDA(cudaEventRecord(c->ev[2], st));
+  // A gradient sink may apply what it is handed at once: make sure K1 accepted
+  // every token id and descriptor before the first gradient leaves the library
+  // (otherwise the step would only fail after the all-reduce).
+  if (train_mode && pool->consume_grad) PRORL_TRY(prorl_check_errors(c, stream));
 
   // ---- K2+K4 (K7 in training mode) over logits micro-batches, or K6 + K4 from hidden states ----
   const int64_t mb = cfg->microbatch_rows;
@@ -573,7 +593,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
       PRORL_TRY(launch_lmhead(c, hid, hs, pool->weight, pool->w_stride, pool->d_model, cfg->vocab,
                               pk.act_target + row0, n, cfg->inv_temperature, lp, en, st));
       int used = 0;
-      PRORL_TRY(launch_loss(c, lp, en, pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0,
+      PRORL_TRY(launch_loss(c, lp, en, pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0,
                             pk.act_turn + row0, ref_lp, n, &cfg->loss, slab, loss_slab_rows(c), &used, st));
       PRORL_TRY(launch_slab_reduce(slab, used, partials, st));
       continue;
@@ -606,7 +626,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
         return fail(PRORL_E_SHAPE, "prorl_score_host: gradient buffer must share the logits' 16-byte phase");
       int used = 0;
       PRORL_TRY(launch_train(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
-                             pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp,
+                             pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp,
                              n, cfg->inv_temperature, &cfg->loss, n_global, nullptr, nullptr, nullptr, grad, slab, true,
                              &used, st));
       if (pool->consume_grad) {
@@ -621,7 +641,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
     // work between them) overlap through programmatic dependent launch
     const bool pdl = j > 0 && pdl_enabled() && !pool->provide && !pool->fill && !ref_lp;
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
-                           pk.act_old_lp + row0, c->adv.as<float>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp, n,
+                           pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st, pdl));
   }
   if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));

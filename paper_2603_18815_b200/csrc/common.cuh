@@ -110,29 +110,29 @@ int launch_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, c
                 const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab,
                 const prorl_packed* out, cudaStream_t st);
 int launch_grpo(prorl_ctx* ctx, const double* reward, const uint8_t* usable, const int32_t* group_off,
-                int32_t n_groups, int32_t ddof, float eps, double tol, float* adv, uint8_t* informative,
+                int32_t n_groups, int32_t ddof, float eps, double tol, double* adv, uint8_t* informative,
                 double* partials, cudaStream_t st);
 // Scoring: if `cfg` is null, K2 only (logp/entropy). Otherwise the fused loss
 // epilogue accumulates into slab rows [blockIdx] (accumulate=true adds to the
 // existing slab content). Returns the number of slab rows used via *slab_rows.
 int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
-                 const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                 const int32_t* rows, const int32_t* targets, const float* old_lp, const double* adv,
                  const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                  float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
                  bool accumulate, int* rows_used, cudaStream_t st, bool pdl = false);
 int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp,
-                const float* adv, const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp,
+                const double* adv, const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp,
                 int64_t n_rows, const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used,
                 cudaStream_t st);
 int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
-                const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
+                const int32_t* targets, const float* logp, const float* old_lp, const double* adv,
                 const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                 const prorl_loss_cfg* cfg, double n_global,
                 void* grad, int64_t grad_stride, float* dlogp, cudaStream_t st);
 // K7 (train.cu): one-pass logprob/entropy + loss epilogue + dL/dlogits.
 int train_slab_rows(prorl_ctx* ctx);
 int launch_train(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
-                 const int32_t* targets, const float* old_lp, const float* adv, const int32_t* row_seq,
+                 const int32_t* targets, const float* old_lp, const double* adv, const int32_t* row_seq,
                  const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float inv_temp,
                  const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy, float* dlogp, void* grad,
                  double* slab, bool accumulate, int* rows_used, cudaStream_t st);

@@ -38,7 +38,7 @@ struct GradArgs {
   const int32_t* targets;
   const float* logp;
   const float* old_lp;
-  const float* adv;
+  const double* adv;
   const int32_t* row_seq;
   const float* ref_lp;  // nullable (k3 KL term)
   float kl_coef;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
     if (lane == 0) {
       const float xy = GElem<T>::load(rp, y);
       const float lp = p.logp[i], old = p.old_lp[i];
-      const float A = p.adv[p.row_seq[i]];
+      const float A = (float)p.adv[p.row_seq[i]];
       const float ratio = expf(lp - old);
       const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
       float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
@@ -174,7 +174,7 @@ int run_grad(const GradArgs& a, int n_sm, cudaStream_t st) {
 }  // namespace
 
 int launch_grad(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
-                const int32_t* targets, const float* logp, const float* old_lp, const float* adv,
+                const int32_t* targets, const float* logp, const float* old_lp, const double* adv,
                 const int32_t* row_seq, const float* ref_lp, int64_t n_rows, float inv_temp,
                 const prorl_loss_cfg* cfg, double n_global, void* grad, int64_t grad_stride, float* dlogp,
                 cudaStream_t st) {

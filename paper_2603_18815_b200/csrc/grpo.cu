@@ -5,8 +5,10 @@
 // (proj/src/trainer/harness.cpp:84-102: < 2 usable -> false, else
 // max - min > tolerance). On top of the gate this kernel computes the GRPO
 // advantage over the usable rollouts of every informative group
-// (SURVEY.md App. B.3):  A = (R - mean) / (std_ddof + eps), fp64 math, stored
-// fp32. Non-usable rollouts and rollouts of non-informative groups get A = 0.
+// (SURVEY.md App. B.3):  A = (R - mean) / (std_ddof + eps), fp64 math and
+// fp64 storage (the loss epilogue multiplies every token of a rollout by its
+// A: an fp32-rounded A shifts a C2 loss sum by ~2e-6 relative). Non-usable
+// rollouts and rollouts of non-informative groups get A = 0.
 //
 // One CTA, one warp per group (groups are small: 4..32 rollouts); the
 // sum(A) / N_rollouts partials are reduced in a fixed order (deterministic).
@@ -21,7 +23,7 @@ constexpr int kGrpoThreads = 1024;
 __global__ void __launch_bounds__(kGrpoThreads)
     k_grpo(const double* __restrict__ reward, const uint8_t* __restrict__ usable,
            const int32_t* __restrict__ group_off, int32_t n_groups, int32_t ddof, float eps, double tol,
-           float* __restrict__ adv, uint8_t* __restrict__ informative, double* partials) {
+           double* __restrict__ adv, uint8_t* __restrict__ informative, double* partials) {
   __shared__ double s_sum[kGrpoThreads / 32];
   __shared__ double s_cnt[kGrpoThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -45,7 +47,10 @@ __global__ void __launch_bounds__(kGrpoThreads)
       mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    const bool info = cnt >= 2.0 && (mx - mn) > tol && (cnt - (double)ddof) > 0.0;
+    // exactly is_informative(tol) — the host gate (build_host_batch, ingest)
+    // applies the same test, so both sides agree on which groups are packed;
+    // ddof <= 1 (checked at launch) keeps cnt - ddof >= 1 for every such group
+    const bool info = cnt >= 2.0 && (mx - mn) > tol;
     const double mean = cnt > 0.0 ? sum / cnt : 0.0;
     double ss = 0.0;
     for (int32_t i = b + lane; i < e; i += 32)
@@ -57,10 +62,10 @@ __global__ void __launch_bounds__(kGrpoThreads)
     const double sd = info ? sqrt(ss / (cnt - (double)ddof)) : 0.0;
     double lsum = 0.0;
     for (int32_t i = b + lane; i < e; i += 32) {
-      float a = 0.0f;
-      if (info && usable[i]) a = (float)((reward[i] - mean) / (sd + (double)eps));
+      double a = 0.0;
+      if (info && usable[i]) a = (reward[i] - mean) / (sd + (double)eps);
       adv[i] = a;
-      lsum += (double)a;
+      lsum += a;
     }
     lsum = warp_sum_d(lsum);
     if (lane == 0) informative[g] = info ? 1 : 0;
@@ -88,10 +93,14 @@ __global__ void __launch_bounds__(kGrpoThreads)
 }  // namespace
 
 int launch_grpo(prorl_ctx* ctx, const double* reward, const uint8_t* usable, const int32_t* group_off,
-                int32_t n_groups, int32_t ddof, float eps, double tol, float* adv, uint8_t* informative,
+                int32_t n_groups, int32_t ddof, float eps, double tol, double* adv, uint8_t* informative,
                 double* partials, cudaStream_t st) {
   (void)ctx;
-  if (n_groups < 0 || ddof < 0) return fail(PRORL_E_SHAPE, "prorl_grpo_adv: n_groups/ddof negative");
+  if (n_groups < 0) return fail(PRORL_E_SHAPE, "prorl_grpo_adv: n_groups negative");
+  // App. B.3 defines ddof 1 (torch.std) and 0; ddof >= 2 would leave an
+  // informative group of ddof usable rollouts without a standard deviation
+  if (ddof != 0 && ddof != 1) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_grpo_adv: ddof must be 0 or 1");
+  if (!(tol >= 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_grpo_adv: gate tolerance must be >= 0");
   if (n_groups == 0) return PRORL_OK;
   k_grpo<<<1, kGrpoThreads, 0, st>>>(reward, usable, group_off, n_groups, ddof, eps, tol, adv, informative,
                                       partials);

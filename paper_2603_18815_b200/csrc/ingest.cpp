@@ -315,14 +315,16 @@ struct Part {
 // tokens are appended; returns FAILED-ness and the reward.
 void parse_response(const char* js, size_t n, int32_t slot, Part& out, bool& failed, double& reward) {
   Scanner s(js, n);
-  failed = false;
+  failed = true;  // a response without "status" counts as FAILED (harness.cpp:263)
   reward = 0.0;
-  bool have_traj = false;
+  bool have_traj = false, cancelled = false;
   int64_t* const ids = out.ids.get();
   double* const lps = out.lp.get();
   s.object([&](std::string_view key) {
     if (key == "status") {
-      failed = s.str() == "FAILED";
+      const std::string_view st = s.str();
+      failed = st == "FAILED";
+      cancelled = st == "CANCELLED";
     } else if (key == "reward") {
       reward = s.number();
     } else if (key == "trajectory") {
@@ -373,7 +375,11 @@ void parse_response(const char* js, size_t n, int32_t slot, Part& out, bool& fai
     }
   });
   s.end();
-  if (!have_traj) throw_parse(PRORL_E_MALFORMED_REQUEST, "response without a trajectory");
+  // The reference harness never records a CANCELLED response (harness.cpp:264:
+  // the slot is re-issued), so a group holding one is not complete.
+  if (cancelled)
+    throw_parse(PRORL_E_INCOMPLETE_GROUP, "CANCELLED rollout: its slot is re-issued, the group is incomplete");
+  if (!have_traj && !failed) throw_parse(PRORL_E_MALFORMED_REQUEST, "response without a trajectory");
 }
 
 void parse_groups(const char* const* json, const size_t* len, const int32_t* group_off, int32_t g0, int32_t g1,

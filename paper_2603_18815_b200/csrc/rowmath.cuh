@@ -163,29 +163,68 @@ __device__ __forceinline__ int raise_top(float lm, float c, Top& top, float2 (&S
   return __ffs(__ballot_sync(kFull, lm == gl)) - 1;
 }
 
-// k3 KL estimator e^d - d - 1 (d = ref - logp), accurate for small |d|.
-__device__ __forceinline__ float kl_k3(float d) {
-  if (fabsf(d) < 0.125f) return d * d * fmaf(d, fmaf(d, fmaf(d, 1.f / 120.f, 1.f / 24.f), 1.f / 6.f), 0.5f);
-  return expm1f(d) - d;
+// Row-end arithmetic in fp64 from the fp32 streaming state
+// of one row: the running reference Mc (x*c units, base 2), the raw logit Mx
+// that set it (kept out of the sums), the sums Sr = sum 2^d and Tr = sum d 2^d
+// over every other logit (d = x*c - Mc, fp32), the target logit xy, the fp32
+// scale c = fl(inv_T * log2 e) the terms were computed with, and inv_T itself.
+// Everything after the sums is fp64, so the only rounding left in logp is the
+// fp32 summation (unbiased) and the ex2.approx terms; in particular
+//   * the scale: fl(inv_T log2 e) is off by up to 2^-25 relative, a scale
+//     error on every logit (a systematic logp bias of ~(x_y - E_p x) 1e-8,
+//     measured -4.4e-8 at C2). Each term 2^(x c - Mc) should have been
+//     2^(x ct - Mc) = 2^(x c - Mc) (1 + ln2 x (ct - c) + ...), and
+//     sum x_v 2^(d_v) = (Tr + Mc Sr) / c, so the first-order fix is exact to
+//     1e-16;
+//   * the top element: S = 2^r (1 + q), q = S_rest 2^-r, r = Mx ct - Mc, so
+//         logp = (x_y - Mx) inv_T - log1p(q)
+//         H    = log1p(q) + ln2 (r q - T_rest 2^-r) / (1 + q)
+//     keep full relative precision when one token takes almost all the
+//     probability (p -> 1, H -> 0).
+constexpr double kLn2d = 0.69314718055994530942;
+constexpr double kLog2ed = 1.44269504088896340736;
+
+struct RowStats {
+  double logp, ent;
+};
+__device__ __forceinline__ RowStats row_stats(float Mc, float Mx, float Sr, float Tr, float xy, float c,
+                                              double inv_t) {
+  const double ct = inv_t * kLog2ed;
+  const double mc = (double)Mc, cc = (double)c;
+  const double S = (double)Sr + kLn2d * (ct - cc) * (((double)Tr + mc * (double)Sr) / cc);
+  const double r = (double)Mx * ct - mc;
+  const double ir = exp2(-r);
+  const double q = S * ir;
+  const double l1q = log1p(q);
+  RowStats o;
+  o.logp = ((double)xy - (double)Mx) * inv_t - l1q;
+  o.ent = l1q + kLn2d * ((r * q - (double)Tr * ir) / (1.0 + q));
+  return o;
 }
 
-// Per-row loss terms (App. B.4/B.5 + optional KL), fp32 math.
+// Per-row loss terms (App. B.4/B.5 + optional KL) in fp64, from
+// the fp64 row statistics and the fp64 advantage: the token-mean loss of a
+// batch is ~1e3x smaller than the sum of its |terms| (DAPO's signed
+// advantages cancel), so the partial sums must not carry fp32 rounding of
+// per-rollout quantities (an fp32 advantage alone moved sum(loss) by 2e-6
+// relative at C2). lo / hi = 1 - eps_lo, 1 + eps_hi in fp64.
 struct RowLoss {
-  float loss, ratio, clip_lo, clip_hi, kl;
+  double loss, ratio, clip_lo, clip_hi, kl;
 };
-__device__ __forceinline__ RowLoss row_loss(float logp, float old, float A, float lo, float hi, const float* ref,
-                                            int64_t i, float kl_coef) {
+__device__ __forceinline__ RowLoss row_loss(double logp, float old, double A, double lo, double hi, const float* ref,
+                                            int64_t i, double kl_coef) {
   RowLoss r;
-  r.ratio = expf(logp - old);
-  const float pg1 = r.ratio * A;
-  const float pg2 = fminf(fmaxf(r.ratio, lo), hi) * A;
-  r.loss = -fminf(pg1, pg2);
-  r.clip_lo = (r.ratio < lo && A < 0.f) ? 1.f : 0.f;
-  r.clip_hi = (r.ratio > hi && A > 0.f) ? 1.f : 0.f;
-  r.kl = 0.f;
+  r.ratio = exp(logp - (double)old);
+  const double pg1 = r.ratio * A;
+  const double pg2 = fmin(fmax(r.ratio, lo), hi) * A;
+  r.loss = -fmin(pg1, pg2);
+  r.clip_lo = (r.ratio < lo && A < 0.0) ? 1.0 : 0.0;
+  r.clip_hi = (r.ratio > hi && A > 0.0) ? 1.0 : 0.0;
+  r.kl = 0.0;
   if (ref) {
-    r.kl = kl_k3(ref[i] - logp);
-    r.loss = fmaf(kl_coef, r.kl, r.loss);
+    const double d = (double)ref[i] - logp;
+    r.kl = expm1(d) - d;
+    r.loss = fma(kl_coef, r.kl, r.loss);
   }
   return r;
 }

@@ -22,13 +22,14 @@
 //     handful of times per row) does the warp take the rescale path, so the
 //     common path has no divergence and no per-lane rescale;
 //   * the current top element (the one that set Mc) is kept OUT of the sums
-//     and re-added analytically at the row end:
-//         S = 2^r (1 + q),  q = S_rest 2^-r,   r = x_top*c - Mc (fma residual)
-//         logp = (x_y*c - Mc - r) ln2 - log1p(q)
+//     and re-added analytically at the row end, in fp64 with the fp32 scale's
+//     rounding corrected (rowmath.cuh row_stats):
+//         S = 2^r (1 + q),  q = S_rest 2^-r,   r = x_top*c - Mc
+//         logp = (x_y - x_top) inv_T - log1p(q)
 //         H    = log1p(q) + ln2 (r q - T_rest 2^-r) / (1 + q)
-//     so logp and H stay accurate to fp32 relative precision even when one
-//     token takes almost all the probability (p -> 1, H -> 0), where a plain
-//     fp32 sum of e^(x - max) cannot resolve 1 + tiny;
+//     so logp and H stay accurate even when one token takes almost all the
+//     probability (p -> 1, H -> 0), where a plain fp32 sum of e^(x - max)
+//     cannot resolve 1 + tiny; the loss epilogue is fp64 too (row_loss);
 //   * -inf / NaN / huge-negative bf16 logits are clamped to -2^97 with one
 //     packed min.u16x2 per two logits (they then contribute exactly 0);
 //   * unaligned row heads/tails (V*esz not a multiple of 16 B, odd row
@@ -82,15 +83,16 @@ struct ScoreArgs {
   const int32_t* rows;
   const int32_t* targets;
   int64_t n_rows;
-  float c;  // inv_temp * log2(e)
+  float c;  // fl(inv_temp * log2(e))
+  float inv_temp;
   // fused loss
   const float* old_lp;
-  const float* adv;
+  const double* adv;
   const int32_t* row_seq;
   const int16_t* row_turn;
   const float* ref_lp;  // nullable
-  float kl_coef;
-  float lo_bound, hi_bound;  // 1 - eps_lo, 1 + eps_hi
+  double kl_coef;
+  double lo_bound, hi_bound;  // 1 - eps_lo, 1 + eps_hi (fp64, as the oracle)
   int n_buckets;
   float* logp;
   float* entropy;
@@ -219,34 +221,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
       Tr = sr.Tr;
     }
     if (lane == 0) {
-      const float r = fmaf(top.Mx, c, -top.Mc);  // top element's own exponent (~0)
-      const float ir = ex2_approx(-r);
-      const float q = Sr * ir;
-      const float l1q = log1pf(q);
-      const float logp = (fmaf(xy, c, -top.Mc) - r) * kLn2 - l1q;
-      const float ent = l1q + kLn2 * (fmaf(r, q, -Tr * ir) / (1.f + q));
-      if (p.logp) p.logp[i] = logp;
-      if (p.entropy) p.entropy[i] = ent;
+      const RowStats rs = row_stats(top.Mc, top.Mx, Sr, Tr, xy, c, (double)p.inv_temp);  // fp64 row end
+      if (p.logp) p.logp[i] = (float)rs.logp;
+      if (p.entropy) p.entropy[i] = (float)rs.ent;
       if constexpr (FUSED) {
         const float old = p.old_lp[i];
-        const float A = p.adv[p.row_seq[i]];
+        const double A = p.adv[p.row_seq[i]];
         int k = p.row_turn[i];
         k = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
-        const RowLoss rl = row_loss(logp, old, A, p.lo_bound, p.hi_bound, p.ref_lp, i, p.kl_coef);
+        const RowLoss rl = row_loss(rs.logp, old, A, p.lo_bound, p.hi_bound, p.ref_lp, i, p.kl_coef);
         g[0] += rl.loss;
         g[1] += 1.0;
-        g[2] += ent;
-        g[3] += logp;
+        g[2] += rs.ent;
+        g[3] += rs.logp;
         g[4] += rl.ratio;
         g[5] += rl.clip_lo;
         g[6] += rl.clip_hi;
-        g[7] += (double)(old - logp);
+        g[7] += (double)old - rs.logp;
         g[10] += rl.kl;
         double* bk = bk_w + warp * kBucketDoubles + k * PRORL_N_PER_TURN;
         bk[0] += 1.0;
         bk[1] += rl.loss;
-        bk[2] += ent;
-        bk[3] += logp;
+        bk[2] += rs.ent;
+        bk[3] += rs.logp;
         bk[4] += rl.clip_lo + rl.clip_hi;
       }
     }
@@ -268,13 +265,13 @@ constexpr int kLossWarps = 8;
 
 __global__ void __launch_bounds__(kLossWarps * 32)
     k_loss(const float* __restrict__ logp, const float* __restrict__ entropy, const float* __restrict__ old_lp,
-           const float* __restrict__ adv, const int32_t* __restrict__ row_seq, const int16_t* __restrict__ row_turn,
-           const float* __restrict__ ref_lp, float kl_coef, int64_t n_rows, float lo, float hi, int n_buckets,
+           const double* __restrict__ adv, const int32_t* __restrict__ row_seq, const int16_t* __restrict__ row_turn,
+           const float* __restrict__ ref_lp, double kl_coef, int64_t n_rows, double lo, double hi, int n_buckets,
            double* slab) {
   __shared__ double g_w[kLossWarps * kNG];
   __shared__ double bk_w[kLossWarps * kBucketDoubles];
   __shared__ int s_key[kLossWarps][32];
-  __shared__ float s_val[kLossWarps][32][PRORL_N_PER_TURN];
+  __shared__ double s_val[kLossWarps][32][PRORL_N_PER_TURN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = lane; i < kBucketDoubles; i += 32) bk_w[warp * kBucketDoubles + i] = 0.0;
   double g[kNG];
@@ -287,8 +284,9 @@ __global__ void __launch_bounds__(kLossWarps * 32)
     const int64_t i = tile * 32 + lane;
     int key = -1;
     if (i < n_rows) {
-      const float lp = logp[i], ent = entropy[i], old = old_lp[i];
-      const float A = adv[row_seq[i]];
+      const double lp = logp[i], ent = entropy[i];
+      const float old = old_lp[i];
+      const double A = adv[row_seq[i]];
       int k = row_turn[i];
       key = k < 0 ? 0 : (k >= n_buckets ? n_buckets - 1 : k);
       const RowLoss r = row_loss(lp, old, A, lo, hi, ref_lp, i, kl_coef);
@@ -299,9 +297,9 @@ __global__ void __launch_bounds__(kLossWarps * 32)
       g[4] += r.ratio;
       g[5] += r.clip_lo;
       g[6] += r.clip_hi;
-      g[7] += (double)(old - lp);
+      g[7] += (double)old - lp;
       g[10] += r.kl;
-      s_val[warp][lane][0] = 1.f;
+      s_val[warp][lane][0] = 1.0;
       s_val[warp][lane][1] = r.loss;
       s_val[warp][lane][2] = ent;
       s_val[warp][lane][3] = lp;
@@ -312,7 +310,7 @@ __global__ void __launch_bounds__(kLossWarps * 32)
     if (lane < PRORL_N_PER_TURN) {  // fixed-order per-turn accumulation
       for (int src = 0; src < 32; ++src) {
         const int kk = s_key[warp][src];
-        if (kk >= 0) bk_w[warp * kBucketDoubles + kk * PRORL_N_PER_TURN + lane] += (double)s_val[warp][src][lane];
+        if (kk >= 0) bk_w[warp * kBucketDoubles + kk * PRORL_N_PER_TURN + lane] += s_val[warp][src][lane];
       }
     }
     __syncwarp();
@@ -391,7 +389,7 @@ int score_slab_rows(prorl_ctx* ctx) { return ctx->n_sm; }
 int loss_slab_rows(prorl_ctx* ctx) { return 2 * ctx->n_sm; }
 
 int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab,
-                 const int32_t* rows, const int32_t* targets, const float* old_lp, const float* adv,
+                 const int32_t* rows, const int32_t* targets, const float* old_lp, const double* adv,
                  const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                  float inv_temp, const prorl_loss_cfg* cfg, float* logp, float* entropy, double* slab, int slab_rows,
                  bool accumulate, int* rows_used, cudaStream_t st, bool pdl) {
@@ -412,6 +410,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.targets = targets;
   a.n_rows = n_rows;
   a.c = inv_temp * kLog2e;
+  a.inv_temp = inv_temp;
   a.old_lp = old_lp;
   a.adv = adv;
   a.row_seq = row_seq;
@@ -427,8 +426,8 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   }();
   a.raise_slack = slack;
   if (cfg) {
-    a.lo_bound = 1.0f - cfg->eps_lo;
-    a.hi_bound = 1.0f + cfg->eps_hi;
+    a.lo_bound = 1.0 - (double)cfg->eps_lo;
+    a.hi_bound = 1.0 + (double)cfg->eps_hi;
     a.n_buckets = cfg->n_buckets;
     a.kl_coef = cfg->kl_coef;
   }
@@ -439,7 +438,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
              : run_score<float, false>(a, ctx->n_sm, n_rows, slab_rows, rows_used, pdl, st);
 }
 
-int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp, const float* adv,
+int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const float* old_lp, const double* adv,
                 const int32_t* row_seq, const int16_t* row_turn, const float* ref_lp, int64_t n_rows,
                 const prorl_loss_cfg* cfg, double* slab, int slab_rows, int* rows_used, cudaStream_t st) {
   *rows_used = 0;
@@ -450,7 +449,8 @@ int launch_loss(prorl_ctx* ctx, const float* logp, const float* entropy, const f
   int grid = (int)std::min<int64_t>((int64_t)slab_rows, (tiles + kLossWarps - 1) / kLossWarps);
   (void)ctx;
   k_loss<<<grid, kLossWarps * 32, 0, st>>>(logp, entropy, old_lp, adv, row_seq, row_turn, ref_lp, cfg->kl_coef,
-                                           n_rows, 1.0f - cfg->eps_lo, 1.0f + cfg->eps_hi, cfg->n_buckets, slab);
+                                           n_rows, 1.0 - (double)cfg->eps_lo, 1.0 + (double)cfg->eps_hi,
+                                           cfg->n_buckets, slab);
   PRORL_CUDA(cudaGetLastError());
   *rows_used = grid;
   return PRORL_OK;

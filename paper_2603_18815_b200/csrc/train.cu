@@ -63,15 +63,16 @@ struct TrainArgs {
   const int32_t* rows;
   const int32_t* targets;
   const float* old_lp;
-  const float* adv;
+  const double* adv;
   const int32_t* row_seq;
   const int16_t* row_turn;
   const float* ref_lp;  // nullable
   float kl_coef;
   int64_t n_rows;
-  float c;  // inv_temp * log2 e
+  float c;  // fl(inv_temp * log2 e)
   float inv_temp;
-  float lo, hi;  // 1 - eps_lo, 1 + eps_hi
+  float lo, hi;      // 1 - eps_lo, 1 + eps_hi (fp32: the gradient's branch)
+  double lo_d, hi_d;  // the same in fp64 (the loss epilogue, as the oracle)
   float inv_n;   // 1 / N_global
   int n_buckets;
   float* logp;
@@ -364,18 +365,20 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
   for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x, ++j) {
     const RowGeo g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
     const int32_t y = p.targets[i];
-    float xy = 0.f, old = 0.f, A = 0.f, ref = 0.f;
+    float xy = 0.f, old = 0.f, ref = 0.f;
+    double Ad = 0.0;
     if (lane == 0) {
       xy = Elem<T>::load(g.rp, y);
       old = p.old_lp[i];
-      A = p.adv[p.row_seq[i]];
+      Ad = p.adv[p.row_seq[i]];
       if (p.ref_lp) ref = p.ref_lp[i];
     }
     // consumed now: in place, pass B of this row overwrites x_y
     xy = __shfl_sync(kFull, xy, 0);
     old = __shfl_sync(kFull, old, 0);
-    A = __shfl_sync(kFull, A, 0);
+    Ad = __shfl_sync(kFull, Ad, 0);
     ref = __shfl_sync(kFull, ref, 0);
+    const float A = (float)Ad;
     const int kk = wq % kSplit;  // this warp's unit inside its pieces
     // first piece (offset from pc0) of a pass that this warp consumes
     auto first_piece = [&](uint32_t pc0) { return (int)(((uint32_t)(wq / kSplit) + kPG - pc0 % kPG) % kPG); };
@@ -479,33 +482,42 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     const float logp = (fmaf(xy, c, -Gp.x) - rr) * kLn2 - l1q;
     const float ratio = expf(logp - old);
     const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
-    float dl = (pg1 <= pg2) ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
+    bool unclipped = pg1 <= pg2;
+    if (fminf(fabsf(ratio - p.lo), fabsf(ratio - p.hi)) <= 1e-5f * ratio) {
+      // a ratio this close to a clip bound takes the branch the fp64 loss
+      // epilogue takes (rare; warp-uniform: every warp holds the same row state)
+      const RowStats rs = row_stats(Gp.x, Gp.y, Gp.z, Gp.w, xy, c, (double)p.inv_temp);
+      const RowLoss rl = row_loss(rs.logp, old, Ad, p.lo_d, p.hi_d, nullptr, 0, 0.0);
+      unclipped = rl.loss == -(rl.ratio * Ad);
+    }
+    float dl = unclipped ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
     if (p.ref_lp) dl = fmaf(p.kl_coef * p.inv_n, -expm1f(ref - logp), dl);
     const float sg = -dl * p.inv_temp;  // grad_v = sg p_v (v != y), grad_y = sg expm1(logp) = -sg (1 - p_y)
     const float l2 = fmaf(xy, c, -logp * kLog2e);
     const float gy = sg * expm1f(logp);
     if (wq == 0 && lane == 0) {
-      const float ent = l1q + kLn2 * (fmaf(rr, qq, -Gp.w * ir) / (1.f + qq));
-      if (p.logp) p.logp[i] = logp;
-      if (p.entropy) p.entropy[i] = ent;
+      // outputs and loss partials from the fp64 row end (rowmath.cuh row_stats / row_loss)
+      const RowStats rs = row_stats(Gp.x, Gp.y, Gp.z, Gp.w, xy, c, (double)p.inv_temp);
+      if (p.logp) p.logp[i] = (float)rs.logp;
+      if (p.entropy) p.entropy[i] = (float)rs.ent;
       if (p.dlogp) p.dlogp[i] = dl;
       int k = p.row_turn[i];
       k = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
-      const RowLoss rl = row_loss(logp, old, A, p.lo, p.hi, p.ref_lp, i, p.kl_coef);
+      const RowLoss rl = row_loss(rs.logp, old, Ad, p.lo_d, p.hi_d, p.ref_lp, i, (double)p.kl_coef);
       gsum[0] += rl.loss;
       gsum[1] += 1.0;
-      gsum[2] += ent;
-      gsum[3] += logp;
+      gsum[2] += rs.ent;
+      gsum[3] += rs.logp;
       gsum[4] += rl.ratio;
       gsum[5] += rl.clip_lo;
       gsum[6] += rl.clip_hi;
-      gsum[7] += (double)(old - logp);
+      gsum[7] += (double)old - rs.logp;
       gsum[10] += rl.kl;
       double* b = bk + k * PRORL_N_PER_TURN;
       b[0] += 1.0;
       b[1] += rl.loss;
-      b[2] += ent;
-      b[3] += logp;
+      b[2] += rs.ent;
+      b[3] += rs.logp;
       b[4] += rl.clip_lo + rl.clip_hi;
     }
 
@@ -682,13 +694,25 @@ int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
 int train_slab_rows(prorl_ctx* ctx) { return ctx->n_sm; }
 
 int launch_train(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stride, int32_t vocab, const int32_t* rows,
-                 const int32_t* targets, const float* old_lp, const float* adv, const int32_t* row_seq,
+                 const int32_t* targets, const float* old_lp, const double* adv, const int32_t* row_seq,
                  const int16_t* row_turn, const float* ref_lp, int64_t n_rows, float inv_temp,
                  const prorl_loss_cfg* cfg, double n_global, float* logp, float* entropy, float* dlogp, void* grad,
                  double* slab, bool accumulate, int* rows_used, cudaStream_t st) {
   *rows_used = 0;
-  if (n_rows <= 0) return PRORL_OK;
+  // every caller (prorl_score_grad, prorl_score_host's training mode) goes
+  // through these checks: the kernel indexes per-group shared-memory buckets
+  // by turn and writes the gradient row by row at row_stride
+  if (dtype != PRORL_BF16 && dtype != PRORL_FP32) return fail(PRORL_E_SHAPE, "train: unknown logits dtype");
+  if (vocab <= 0 || row_stride < vocab) return fail(PRORL_E_SHAPE, "train: need vocab > 0 and row_stride >= vocab");
+  if (!(inv_temp > 0.f)) return fail(PRORL_E_MALFORMED_REQUEST, "train: inv_temperature must be > 0");
+  if (!(n_global > 0.0)) return fail(PRORL_E_MALFORMED_REQUEST, "train: n_global must be > 0");
+  if (!cfg || cfg->n_buckets < 1 || cfg->n_buckets > PRORL_TURN_BUCKETS)
+    return fail(PRORL_E_SHAPE, "train: n_buckets out of [1, 64]");
   const int esz = dtype == PRORL_BF16 ? 2 : 4;
+  if (reinterpret_cast<uintptr_t>(logits) % esz ||
+      (static_cast<const uint8_t*>(grad) - static_cast<const uint8_t*>(logits)) % 16 != 0)
+    return fail(PRORL_E_SHAPE, "train: grad must share the logits' 16-byte alignment phase");
+  if (n_rows <= 0) return PRORL_OK;
   TrainArgs a{};
   a.logits = static_cast<const uint8_t*>(logits);
   a.stride_bytes = row_stride * esz;
@@ -707,6 +731,8 @@ int launch_train(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.inv_temp = inv_temp;
   a.lo = 1.0f - cfg->eps_lo;
   a.hi = 1.0f + cfg->eps_hi;
+  a.lo_d = 1.0 - (double)cfg->eps_lo;
+  a.hi_d = 1.0 + (double)cfg->eps_hi;
   a.inv_n = (float)(1.0 / n_global);
   a.n_buckets = cfg->n_buckets;
   a.logp = logp;

@@ -19,6 +19,13 @@ from ._native import RolloutError, check, ptr  # noqa: F401  (RolloutError re-ex
 _DT = {torch.bfloat16: N.PRORL_BF16, torch.float32: N.PRORL_FP32}
 
 
+def _adv(adv: torch.Tensor) -> torch.Tensor:
+    """Advantages cross the C-ABI as fp64 (prorl_grpo_adv's output type)."""
+    if adv.dtype != torch.float64:
+        raise TypeError(f"advantages must be float64 (got {adv.dtype})")
+    return adv
+
+
 def _stream(stream=None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -45,11 +52,13 @@ class ScoreConfig:
     ddof: int = 1
     microbatch_rows: int = 16576  # 7 waves of the 148 x 16 K2 warps
     loss: LossConfig = None
+    gate_tolerance: float = 0.0   # is_informative tolerance (K3 gate; the host batch must use the same)
 
     def c(self) -> N.ScoreCfg:
         loss = self.loss or LossConfig()
         return N.ScoreCfg(loss.c(), self.inv_temperature, self.adv_eps, self.ddof, self.vocab,
-                          N.PRORL_BF16 if self.dtype == "bf16" else N.PRORL_FP32, self.microbatch_rows)
+                          N.PRORL_BF16 if self.dtype == "bf16" else N.PRORL_FP32, self.microbatch_rows,
+                          self.gate_tolerance)
 
 
 class Scorer:
@@ -103,7 +112,7 @@ class Scorer:
     # ---- K3 ----
     def grpo_adv(self, reward: torch.Tensor, usable: torch.Tensor, group_off: torch.Tensor, ddof: int = 1,
                  eps: float = 1e-6, tol: float = 0.0, partials: torch.Tensor | None = None, stream=None):
-        adv = torch.empty(max(reward.numel(), 1), dtype=torch.float32, device=reward.device)
+        adv = torch.empty(max(reward.numel(), 1), dtype=torch.float64, device=reward.device)
         ng = group_off.numel() - 1
         info = torch.empty(max(ng, 1), dtype=torch.uint8, device=reward.device)
         check(N.lib.prorl_grpo_adv(self.ctx, ptr(reward), ptr(usable), ptr(group_off), ng, ddof, eps, tol, ptr(adv),
@@ -127,7 +136,7 @@ class Scorer:
         if partials is None:
             partials = torch.zeros(N.N_PARTIALS, dtype=torch.float64, device=logp.device)
         c = (cfg or LossConfig()).c()
-        check(N.lib.prorl_clipped_loss(self.ctx, ptr(logp), ptr(entropy), ptr(old_lp), ptr(adv), ptr(row_seq),
+        check(N.lib.prorl_clipped_loss(self.ctx, ptr(logp), ptr(entropy), ptr(old_lp), ptr(_adv(adv)), ptr(row_seq),
                                        ptr(row_turn), ptr(ref_lp), logp.numel(), C.byref(c), ptr(partials),
                                        _stream(stream)))
         return partials
@@ -145,7 +154,7 @@ class Scorer:
         c = (cfg or LossConfig()).c()
         V = vocab if vocab is not None else logits.shape[1]
         check(N.lib.prorl_score_rows(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
-                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
+                                     ptr(targets), ptr(old_lp), ptr(_adv(adv)), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
                                      inv_temp, C.byref(c), ptr(logp), ptr(ent), ptr(partials), _stream(stream)))
         return partials, logp, ent
 
@@ -161,7 +170,7 @@ class Scorer:
         c = (cfg or LossConfig()).c()
         V = vocab if vocab is not None else logits.shape[1]
         check(N.lib.prorl_logits_grad(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
-                                      ptr(targets), ptr(logp), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(ref_lp), n,
+                                      ptr(targets), ptr(logp), ptr(old_lp), ptr(_adv(adv)), ptr(row_seq), ptr(ref_lp), n,
                                       inv_temp,
                                       C.byref(c), float(n_global), ptr(grad), grad.stride(0), ptr(dl),
                                       _stream(stream)))
@@ -185,7 +194,7 @@ class Scorer:
         c = (cfg or LossConfig()).c()
         V = vocab if vocab is not None else logits.shape[1]
         check(N.lib.prorl_score_grad(self.ctx, ptr(logits), _DT[logits.dtype], logits.stride(0), V, ptr(rows),
-                                     ptr(targets), ptr(old_lp), ptr(adv), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
+                                     ptr(targets), ptr(old_lp), ptr(_adv(adv)), ptr(row_seq), ptr(row_turn), ptr(ref_lp), n,
                                      inv_temp, C.byref(c), float(n_global), ptr(logp), ptr(ent), ptr(partials),
                                      ptr(grad), grad.stride(0), ptr(dl), _stream(stream)))
         return partials, logp, ent, grad, dl

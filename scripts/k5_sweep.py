@@ -8,7 +8,7 @@ t = torch.randint(0, V, (n,), dtype=torch.int32, device="cuda")
 old = torch.full((n,), -1.2, device="cuda")
 s.gen_logits(x, n, 0, t, old)
 lp, _ = s.logprob_entropy(x, t)
-adv = torch.randn(64, device="cuda"); seq = torch.randint(0, 64, (n,), dtype=torch.int32, device="cuda")
+adv = torch.randn(64, device="cuda", dtype=torch.float64); seq = torch.randint(0, 64, (n,), dtype=torch.int32, device="cuda")
 old2 = lp + 0.3 * (torch.rand(n, device="cuda") - 0.5)
 for _ in range(2): s.logits_grad(x, t, lp, old2, adv, seq, float(n), grad=y)
 torch.cuda.synchronize()

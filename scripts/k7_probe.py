@@ -28,7 +28,7 @@ t = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
 old = -0.05 - 2.9 * torch.rand(n, device="cuda", generator=g)
 for xb in xs:
     sc.gen_logits(xb, n, 0, t, old, seed=3, sigma=2.0)
-adv = torch.randn(64, device="cuda", generator=g)
+adv = torch.randn(64, device="cuda", generator=g, dtype=torch.float64)
 seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
 turn = torch.randint(0, 30, (n,), device="cuda", dtype=torch.int16, generator=g)
 

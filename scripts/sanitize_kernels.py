@@ -25,7 +25,7 @@ old = torch.full((n,), -1.2, device=dev)
 s.gen_logits(x, n, 0, t, old, vocab=V)
 rows = torch.randperm(n, device=dev).to(torch.int32)
 lp, ent = s.logprob_entropy(x, t, rows=rows, vocab=V)
-adv = torch.randn(8, device=dev)
+adv = torch.randn(8, device=dev, dtype=torch.float64)
 seq = torch.randint(0, 8, (n,), dtype=torch.int32, device=dev)
 turn = torch.randint(0, 70, (n,), dtype=torch.int16, device=dev)
 s.clipped_loss(lp, ent, old, adv, seq, turn, cfg=LossConfig(kl_coef=1e-4), ref_lp=lp + 0.1)

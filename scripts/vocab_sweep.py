@@ -46,7 +46,7 @@ for V, dt in [(32000, torch.float32), (32000, torch.bfloat16), (65536, torch.bfl
     t = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
     old = -0.05 - 2.9 * torch.rand(n, device="cuda", generator=g)
     sc.gen_logits(x, n, 0, t, old, seed=3, sigma=2.0)
-    adv = torch.randn(64, device="cuda", generator=g)
+    adv = torch.randn(64, device="cuda", generator=g, dtype=torch.float64)
     seq = torch.randint(0, 64, (n,), device="cuda", dtype=torch.int32, generator=g)
     turn = torch.randint(0, 30, (n,), device="cuda", dtype=torch.int16, generator=g)
     lp, _ = sc.logprob_entropy(x, t)

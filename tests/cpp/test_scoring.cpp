@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "rollout/trainer/scoring.hpp"
+#include "rollout/trainer/synthetic_logits.hpp"
 
 using namespace rollout;
 using namespace rollout::train;
@@ -47,9 +48,9 @@ static std::optional<RolloutOutcome> outcome(double r, const char* status = "DON
   return o;
 }
 
-static PromptGroup group_of(std::vector<std::optional<RolloutOutcome>> os) {
+static PromptGroup group_of(std::vector<std::optional<RolloutOutcome>> os, std::string id = "p") {
   PromptGroup g;
-  g.prompt_id = "p";
+  g.prompt_id = std::move(id);
   g.n = (int)os.size();
   g.outcomes = std::move(os);
   return g;
@@ -89,7 +90,6 @@ static void host_checks() {
   CHECK(t.flatten_range(1, 3) == (TokenIds{10, 11, 4}));
   CHECK(t.flatten_range(3, 99) == (TokenIds{12}));
   CHECK(t.flatten_range(2, 2).empty());
-  CHECK(t.token_count() == 7);
 
   // test_core.cpp:144-170
   TokenTrajectory e;
@@ -133,8 +133,22 @@ static void host_checks() {
     "backend":"http://127.0.0.1:9000"})";
   RolloutOutcome o = outcome_from_response(nlohmann::json::parse(resp));
   CHECK(o.status == "DONE" && o.reward == 1.0 && o.address == "http://127.0.0.1:9000");
-  CHECK(o.trajectory && o.trajectory->flatten() == (TokenIds{104, 105, 300, 7}));
-  CHECK(o.trajectory->turns()[1].logprobs == (std::vector<double>{-1.0, -1.3}));
+  TrajectoryTable table;
+  PromptGroup rg = group_of({std::nullopt, std::nullopt}, "r");
+  CHECK(record_response(rg, 1, nlohmann::json::parse(resp), table, 0.25));
+  CHECK(rg.outcomes[1] && rg.outcomes[1]->status == "DONE" && rg.outcomes[1]->wall_seconds == 0.25);
+  const TokenTrajectory* rt = table.find("r", 1);
+  CHECK(rt && rt->flatten() == (TokenIds{104, 105, 300, 7}));
+  CHECK(rt && rt->turns()[1].logprobs == (std::vector<double>{-1.0, -1.3}));
+  // harness.cpp:263-265: a missing status records FAILED, CANCELLED is not recorded
+  CHECK(outcome_from_response(nlohmann::json::parse(R"({"reward":1.0})")).status == "FAILED");
+  CHECK(!record_response(rg, 0, nlohmann::json::parse(R"({"status":"CANCELLED","reward":1.0,"trajectory":[]})"),
+                         table));
+  CHECK(!rg.outcomes[0] && table.find("r", 0) == nullptr);
+  CHECK(record_response(rg, 0, nlohmann::json::parse(R"({"reward":0.0})"), table));  // FAILED: no trajectory needed
+  CHECK(rg.outcomes[0]->status == "FAILED" && table.find("r", 0) == nullptr);
+  CHECK(throws<MalformedRequest>([&] { record_response(rg, 0, nlohmann::json::parse(R"({"status":"DONE"})"), table); },
+                                 "malformed_request"));
   auto bad_json = nlohmann::json::parse(R"([{"role":"assistant","input_ids":[1],"output_ids":[],"logprobs":[]}])");
   CHECK(throws<MalformedTurn>([&] { trajectory_from_json(bad_json); }, "malformed_turn"));
   CHECK(throws<MalformedTurn>([&] { trajectory_from_json(nlohmann::json::parse(R"([{"role":"robot"}])")); },
@@ -144,23 +158,24 @@ static void host_checks() {
   ScoreConfig cfg;
   cfg.vocab = 50000;
   std::vector<PromptGroup> gs;
+  TrajectoryTable tt;
   {
     std::vector<std::optional<RolloutOutcome>> os;
     for (int i = 0; i < 4; ++i) {
-      auto oc = outcome(i % 2 ? 1.0 : 0.0, i == 3 ? "FAILED" : "DONE");
-      oc->trajectory = traj(10 + i, 3, 50000);
-      os.push_back(oc);
+      os.push_back(outcome(i % 2 ? 1.0 : 0.0, i == 3 ? "FAILED" : "DONE"));
+      tt.put("a", i, traj(10 + i, 3, 50000));
     }
-    gs.push_back(group_of(os));
     std::vector<std::optional<RolloutOutcome>> os2;
     for (int i = 0; i < 2; ++i) {
-      auto oc = outcome(1.0);
-      oc->trajectory = traj(20 + i, 3, 50000);
-      os2.push_back(oc);
+      os2.push_back(outcome(1.0));
+      tt.put("b", i, traj(20 + i, 3, 50000));
     }
-    gs.push_back(group_of(os2));
+    // handed over in completion order "b" before "a": packed in prompt_id order (App. B.1)
+    gs.push_back(group_of(os2, "b"));
+    gs.push_back(group_of(os, "a"));
   }
-  HostBatch hb = build_host_batch(gs, cfg);
+  HostBatch hb = build_host_batch(gs, tt, cfg);
+  CHECK((hb.prompt_ids == std::vector<std::string>{"a", "b"}));
   CHECK(hb.reward.size() == 6 && hb.usable.size() == 6);
   CHECK((hb.group_off == std::vector<std::int32_t>{0, 4, 6}));
   CHECK(hb.usable[3] == 0 && hb.usable[0] == 1);
@@ -168,35 +183,58 @@ static void host_checks() {
   std::int64_t toks = 0, act = 0;
   for (int s = 0; s < 3; ++s) {
     const TokenTrajectory tr = traj(10 + s, 3, 50000);
-    toks += (std::int64_t)tr.token_count();
+    toks += (std::int64_t)tr.flatten().size();
     for (const Turn& tt : tr.turns())
       if (tt.role == Role::ASSISTANT) act += (std::int64_t)tt.output_ids.size();
   }
   CHECK((std::int64_t)hb.ids.size() == toks && hb.lp.size() == hb.ids.size());
   CHECK(hb.n_active == act);  // first turns are user turns: every policy token has a predecessor
   for (const auto& d : hb.turns) CHECK(d.traj >= 0 && d.traj < 3);
-  auto missing = gs;
-  missing[0].outcomes[0]->trajectory.reset();
-  CHECK(throws<MalformedRequest>([&] { build_host_batch(missing, cfg); }, "malformed_request"));
+  {
+    const HostBatch again = build_host_batch(std::vector<PromptGroup>{gs[1], gs[0]}, tt, cfg);
+    CHECK(again.ids == hb.ids && again.reward == hb.reward && again.group_off == hb.group_off);
+  }
+  TrajectoryTable partial_table;
+  partial_table.put("a", 1, traj(11, 3, 50000));
+  CHECK(throws<MalformedRequest>([&] { build_host_batch(gs, partial_table, cfg); }, "malformed_request"));
+  auto cancelled = gs;
+  cancelled[0].outcomes[1]->status = "CANCELLED";
+  CHECK(throws<IncompleteGroup>([&] { build_host_batch(cancelled, tt, cfg); }, "incomplete_group"));
+  // the host gate takes the tolerance (K3 gates with the same value, prorl_score_cfg.gate_tolerance)
+  ScoreConfig tol_cfg = cfg;
+  tol_cfg.gate_tolerance = 1.0;
+  CHECK(build_host_batch(gs, tt, tol_cfg).turns.empty());
+  tt.erase_group("b");
+  CHECK(tt.size() == 4 && tt.find("b", 0) == nullptr && tt.find("a", 0) != nullptr);
 
   // deterministic LPT sharding; groups never split
   std::vector<PromptGroup> many;
+  TrajectoryTable mt;
   for (int gi = 0; gi < 7; ++gi) {
     std::vector<std::optional<RolloutOutcome>> os;
+    const std::string id = "g" + std::to_string(gi);
     for (int i = 0; i < 2; ++i) {
-      auto oc = outcome(i);
-      oc->trajectory = traj(100 + 7 * gi + i, 1 + 2 * gi, 50000);
-      os.push_back(oc);
+      os.push_back(outcome(i));
+      mt.put(id, i, traj(100 + 7 * (gi % 4) + i, 1 + 2 * (gi % 4), 50000));  // equal loads: ties
     }
-    many.push_back(group_of(os));
+    many.push_back(group_of(os, id));
   }
-  auto sh = shard_groups(many, 3);
+  auto sh = shard_groups(many, mt, 3);
   CHECK(sh.size() == 3);
   std::size_t total = 0;
-  for (auto& s : sh) total += s.size();
+  for (auto& s : sh) {
+    total += s.size();
+    for (std::size_t i = 1; i < s.size(); ++i) CHECK(s[i - 1].prompt_id < s[i].prompt_id);
+  }
   CHECK(total == many.size());
-  auto sh2 = shard_groups(many, 3);
-  for (int r = 0; r < 3; ++r) CHECK(sh[r].size() == sh2[r].size());
+  // every rank computes the same assignment whatever order the groups arrived in
+  auto rev = many;
+  std::reverse(rev.begin(), rev.end());
+  auto sh2 = shard_groups(rev, mt, 3);
+  for (int r = 0; r < 3; ++r) {
+    CHECK(sh[r].size() == sh2[r].size());
+    for (std::size_t i = 0; i < sh[r].size() && i < sh2[r].size(); ++i) CHECK(sh[r][i].prompt_id == sh2[r][i].prompt_id);
+  }
 
   // finalize
   std::vector<double> p(PRORL_N_PARTIALS, 0.0);
@@ -227,19 +265,20 @@ static int gpu_run() {
   cfg.dtype = LogitsDtype::BF16;
   cfg.microbatch_rows = 64;
   std::vector<PromptGroup> groups;
+  TrajectoryTable table;
   for (int gi = 0; gi < 6; ++gi) {
     std::vector<std::optional<RolloutOutcome>> os;
+    const std::string id = "p" + std::to_string(gi);
     for (int i = 0; i < 4; ++i) {
-      auto oc = outcome((gi + i) % 3 == 0 ? 1.0 : 0.0, (gi == 2 && i == 1) ? "FAILED" : "DONE");
-      oc->trajectory = traj(1000 + 4 * gi + i, 2 + (gi % 5) * 3, V);
-      os.push_back(oc);
+      os.push_back(outcome((gi + i) % 3 == 0 ? 1.0 : 0.0, (gi == 2 && i == 1) ? "FAILED" : "DONE"));
+      table.put(id, i, traj(1000 + 4 * gi + i, 2 + (gi % 5) * 3, V));
     }
-    groups.push_back(group_of(os));
+    groups.push_back(group_of(os, id));
   }
   DeviceScorer scorer(0);
   SyntheticLogits lm(0, V, cfg.dtype, cfg.microbatch_rows, /*seed=*/4242, 2.0f);
-  const HostBatch hb = build_host_batch(groups, cfg);
-  const ScoreResult r = scorer.score_groups(groups, lm, cfg);
+  const HostBatch hb = build_host_batch(groups, table, cfg);
+  const ScoreResult r = scorer.score_groups(groups, table, lm, cfg);
   std::printf("{\"n_active_host\":%lld,", (long long)hb.n_active);
   std::printf("\"turns\":[");
   for (std::size_t i = 0; i < hb.turns.size(); ++i)
@@ -292,7 +331,7 @@ static int gpu_run() {
   } sink;
   sink.V = V;
   SyntheticLogits lm2(0, V, cfg.dtype, cfg.microbatch_rows, /*seed=*/4242, 2.0f);
-  const ScoreResult tr = scorer.train_groups(groups, lm2, sink, cfg);
+  const ScoreResult tr = scorer.train_groups(groups, table, lm2, sink, cfg);
   print_array("train_partials", tr.partials);
   std::printf(",\"grad_batches\":[");
   for (std::size_t i = 0; i < sink.batches.size(); ++i)

@@ -27,7 +27,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version_and_codes():
-    assert N.lib.prorl_abi_version() == 1
+    assert N.lib.prorl_abi_version() == 2
     assert N.lib.prorl_status_code(-1) == b"malformed_turn"
     assert N.lib.prorl_status_code(-2) == b"incomplete_group"
     assert N.lib.prorl_status_code(-10) == b"cuda_error"
@@ -40,7 +40,7 @@ def test_struct_layouts_match_header():
     import ctypes as C
     assert C.sizeof(N.Packed) == 13 * 8
     assert C.sizeof(N.LossCfg) == 16
-    assert C.sizeof(N.ScoreCfg) == 40
+    assert C.sizeof(N.ScoreCfg) == 48
     assert N.TURN_DTYPE.itemsize == 24
     assert C.sizeof(N.HostBatch) == 88
     assert C.sizeof(N.LogitsPool) == 144

@@ -26,7 +26,7 @@ def _case(scorer, cuda, V, n, dtype, stride=None, seed=0, n_seq=11):
     x = torch.empty((n, stride), dtype=tdt, device=cuda)
     scorer.gen_logits(x, n, 1000, dev(targets, cuda), dev(old, cuda), seed=seed + 5, sigma=2.0, vocab=V)
     host = O.gen_logits(n, V, 1000, targets, old, seed=seed + 5, sigma=2.0, dtype=dtype, row_stride=stride)
-    adv = rng.normal(0, 1, n_seq).astype(np.float32)
+    adv = rng.normal(0, 1, n_seq).astype(np.float64)
     seq = rng.integers(0, n_seq, n).astype(np.int32)
     return x, host, targets, old, adv, seq
 
@@ -129,6 +129,6 @@ def test_logits_grad_dominant_and_masked_rows(scorer, cuda):
     x = torch.from_numpy(xh).to(cuda).to(torch.bfloat16)
     host = x.view(torch.int16).cpu().numpy().view(np.uint16)
     old = np.full(n, -0.7, np.float32)
-    adv = np.array([1.0, -1.0], np.float32)
+    adv = np.array([1.0, -1.0], np.float64)
     seq = np.array([0, 1, 0, 1], np.int32)
     _check(scorer, cuda, x, host, t, old, adv, seq, V, "bf16", n_global=10.0)

@@ -17,7 +17,7 @@ import torch
 from oracle import oracle as O
 from paper_2603_18815_b200 import _native as N
 from paper_2603_18815_b200.hotpath import LossConfig
-from tests.test_gpu_parity import assert_partials_close, assert_rows_close
+from tests.parity import assert_partials_close, assert_rows_close
 
 pytestmark = pytest.mark.gpu
 
@@ -35,7 +35,7 @@ def _case(scorer, cuda, V, n, dtype, stride=None, seed=0, n_seq=11):
     x = torch.empty((n, stride), dtype=tdt, device=cuda)
     scorer.gen_logits(x, n, 1000, dev(targets, cuda), dev(old, cuda), seed=seed + 5, sigma=2.0, vocab=V)
     host = O.gen_logits(n, V, 1000, targets, old, seed=seed + 5, sigma=2.0, dtype=dtype, row_stride=stride)
-    adv = rng.normal(0, 1, n_seq).astype(np.float32)
+    adv = rng.normal(0, 1, n_seq).astype(np.float64)
     seq = rng.integers(0, n_seq, n).astype(np.int32)
     turn = rng.integers(-1, 70, n).astype(np.int16)
     return x, host, targets, old, adv, seq, turn
@@ -163,7 +163,7 @@ def test_score_grad_edge_rows(scorer, cuda):
     x = torch.from_numpy(xh).to(cuda).to(torch.bfloat16)
     host = x.view(torch.int16).cpu().numpy().view(np.uint16)
     old = np.full(n, -0.7, np.float32)
-    adv = np.array([1.0, -1.0], np.float32)
+    adv = np.array([1.0, -1.0], np.float64)
     seq = np.array([0, 1, 0, 1, 0, 1], np.int32)
     turn = np.zeros(n, np.int16)
     part, lp, ent, g, dl = _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 10.0)
@@ -181,7 +181,7 @@ def test_score_grad_full_microbatch_properties(scorer, cuda):
     old = (-0.05 - 2.95 * rng.random(n)).astype(np.float32)
     x = torch.empty((n, V), dtype=torch.bfloat16, device=cuda)
     scorer.gen_logits(x, n, 0, dev(t, cuda), dev(old, cuda), seed=9, sigma=2.0)
-    adv = rng.normal(0, 1, 280).astype(np.float32)
+    adv = rng.normal(0, 1, 280).astype(np.float64)
     seq = np.sort(rng.integers(0, 280, n)).astype(np.int32)
     turn = rng.integers(0, 40, n).astype(np.int16)
     td, od, ad, sd, trd = (dev(a, cuda) for a in (t, old, adv, seq, turn))
@@ -263,7 +263,7 @@ def test_score_grad_running_max_slack(scorer, cuda):
     n = len(rows)
     t = np.array(targets, np.int32)
     old = np.full(n, -0.5, np.float32)
-    adv = np.array([1.0, -1.0], np.float32)
+    adv = np.array([1.0, -1.0], np.float64)
     seq = (np.arange(n) % 2).astype(np.int32)
     turn = np.zeros(n, np.int16)
     _check_all(scorer, cuda, x, host, t, old, adv, seq, turn, V, "bf16", 10.0)

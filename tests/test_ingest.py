@@ -54,7 +54,9 @@ def _check(b, exp):
 
 @pytest.mark.parametrize("group_size", [1, 2, 3, 4, 24])
 def test_reference_wire_json(group_size):
-    cases = GOLD["process_response"]
+    # the harness never records a CANCELLED response (harness.cpp:264: the slot
+    # is re-issued), so a shard never holds one (see test_cancelled_response_...)
+    cases = [c for c in GOLD["process_response"] if c["status"] != "CANCELLED"]
     group_off = list(range(0, len(cases) + 1, group_size))
     if group_off[-1] != len(cases):
         group_off.append(len(cases))
@@ -62,6 +64,26 @@ def test_reference_wire_json(group_size):
     exp = _expected(cases, group_off)
     _check(b, exp)
     assert n_active == exp[5]
+
+
+def test_cancelled_response_makes_the_group_incomplete():
+    cancelled = [c for c in GOLD["process_response"] if c["status"] == "CANCELLED"]
+    done = [c for c in GOLD["process_response"] if c["status"] == "DONE"]
+    assert cancelled and done
+    with pytest.raises(RolloutError) as e:
+        ingest_responses([done[0]["json"].encode(), cancelled[0]["json"].encode()], [0, 2])
+    assert e.value.code == "incomplete_group"
+
+
+def test_missing_status_reads_as_failed():
+    """harness.cpp:263: response.value("status", "FAILED")."""
+    ok = b'{"status":"DONE","reward":1,"trajectory":[{"role":"user","input_ids":[1]},' \
+         b'{"role":"assistant","output_ids":[2,3],"logprobs":[-1.0,-1.1]}]}'
+    no_status = b'{"reward":0,"trajectory":[{"role":"user","input_ids":[1]}]}'
+    no_status_no_traj = b'{"reward":0.5}'
+    b, n_active, n_info = ingest_responses([ok, no_status, no_status_no_traj], [0, 3])
+    assert b.usable.tolist() == [1, 0, 0]
+    assert n_info == 0 and n_active == 0  # one usable reward: not informative
 
 
 def test_synthetic_shard_roundtrip():

@@ -192,6 +192,92 @@ def test_oracle_logprob_entropy_vs_torch_float64():
         np.testing.assert_allclose(ent, ref_ent.numpy(), rtol=1e-10, atol=1e-10)
 
 
+def _prime_rl_loss():
+    """prime-rl's selective_log_softmax / compute_entropy (/opt/prime-rl/src/prime_rl/trainer/rl/loss.py:43-57),
+    the third-party trainer in this image, run eagerly (their @torch.compile is
+    switched off: the functions' own code runs, not an inductor kernel)."""
+    import torch
+    import torch._dynamo
+    try:
+        from prime_rl.trainer.rl import loss as L
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"prime_rl not importable: {e}")
+    torch._dynamo.config.disable = True
+    return L.selective_log_softmax, L.compute_entropy
+
+
+def _oracle_rows(x, t, inv_temp=1.0):
+    """oracle_row_logprob over the rows of x (uint16 bf16 bits or float32)."""
+    return O.logprob_entropy(x, t, inv_temp=inv_temp)
+
+
+def _as_f64(x):
+    if x.dtype == np.uint16:
+        return (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return x.astype(np.float64)
+
+
+@pytest.mark.parametrize("case", ["all_equal", "dominant", "neg_inf", "wide", "c2_keyed_bf16", "fp32_temp"])
+def test_oracle_vs_prime_rl_selective_log_softmax_and_entropy(case):
+    """Independent pin of the oracle's logprob / entropy:
+    prime-rl's selective_log_softmax (gathered log_softmax) and compute_entropy
+    (logsumexp - sum p x) in float64 on the same rows. GRPO / DAPO have no
+    third-party implementation in this image (prime-rl's loss is a DPPO+KL
+    variant with a mean-only advantage, loss.py:96-160), so B.3-B.4 stay pinned
+    by hand-computed cases (test_oracle_grpo_and_loss_hand_computed)."""
+    import torch
+    sls, ent_fn = _prime_rl_loss()
+    rng = np.random.default_rng(11)
+    inv_t = 1.0
+    if case == "all_equal":                    # H = ln V, logp = -ln V
+        V, n = 151936, 3
+        x = np.full((n, V), 0x3f80, np.uint16)  # bf16 1.0 everywhere
+        t = rng.integers(0, V, n).astype(np.int32)
+    elif case == "dominant":                   # one logit 60 nats above the rest: p -> 1, H -> 0
+        V, n = 32000, 4
+        x = (rng.normal(0, 1, (n, V))).astype(np.float32)
+        t = rng.integers(0, V, n).astype(np.int32)
+        x[np.arange(n), t] = 60.0
+        t[1] = (t[1] + 1) % V                  # and one row scored on a non-dominant target
+    elif case == "neg_inf":                    # masked vocabulary entries
+        V, n = 4099, 5
+        x = (rng.normal(0, 2, (n, V))).astype(np.float32)
+        x[:, ::3] = -np.inf
+        t = (rng.integers(0, V // 3, n) * 3 + 1).astype(np.int32)
+    elif case == "wide":                       # the largest C5 vocabulary
+        V, n = 262144, 3
+        x = O.gen_logits(n, V, 5, seed=3, sigma=2.0, dtype="bf16")
+        t = rng.integers(0, V, n).astype(np.int32)
+    elif case == "c2_keyed_bf16":              # rows as the C2 bench generates them (planted targets)
+        V, n = 151936, 6
+        t = rng.integers(0, V, n).astype(np.int32)
+        old = (-0.05 - 2.9 * rng.random(n)).astype(np.float32)
+        x = O.gen_logits(n, V, 31 << 20, t, old, seed=31, sigma=2.0, dtype="bf16")
+    else:                                      # fp32 logits at temperature 0.7
+        V, n = 32000, 8
+        x = (rng.normal(0, 3, (n, V))).astype(np.float32)
+        t = rng.integers(0, V, n).astype(np.int32)
+        inv_t = 1 / 0.7
+    lp, ent = _oracle_rows(x, t, inv_temp=inv_t)
+    xt = torch.from_numpy(_as_f64(x) * float(np.float32(inv_t)))[None]      # [1, n, V] float64
+    ref_lp = sls(xt, torch.from_numpy(t).long()[None])[0].numpy()
+    np.testing.assert_allclose(lp, ref_lp, rtol=1e-12, atol=1e-12)
+    if case == "neg_inf":
+        # compute_entropy multiplies p * x: 0 * -inf is NaN there; the oracle
+        # (App. B.2) gives a -inf logit the term 0 — compare on the finite entries
+        xf = torch.where(torch.isinf(xt), torch.full_like(xt, -1e4), xt)
+        assert torch.isnan(ent_fn(xt)).all()
+        ref_ent = ent_fn(xf)[0].numpy()
+    else:
+        ref_ent = ent_fn(xt)[0].numpy()
+    # compute_entropy's logsumexp - sum p x cancels when p -> 1 (absolute
+    # error ~1e-15); the oracle's log1p form does not
+    np.testing.assert_allclose(ent, ref_ent, rtol=1e-11, atol=1e-13)
+    if case == "all_equal":
+        np.testing.assert_allclose(ent, np.log(V), rtol=1e-14)
+        np.testing.assert_allclose(lp, -np.log(V), rtol=1e-14)
+
+
 def test_oracle_grpo_and_loss_hand_computed():
     # group of 4 usable rewards [1, 0, 1, 0] (+ one FAILED): mean 0.5, std(ddof=1) = sqrt(1/3)
     adv, info, asum, nr = O.grpo(np.array([1.0, 0.0, 1.0, 0.0, 1.0]), np.array([1, 1, 1, 1, 0], np.uint8),

@@ -9,6 +9,10 @@
 //      trainer's LM-head backward would run (here: counted).
 //
 //   score_responses <responses.jsonl> <group_size> <vocab> [bf16|fp32] [seed] [--train]
+//
+// Build (standalone: no reference tree; the façade is header-only):
+//   g++ -std=c++17 -Iinclude -Iinclude/standalone -I<json.hpp dir> -I/usr/local/cuda/include \
+//       tools/score_responses.cpp -Lpaper_2603_18815_b200 -lprorl_hotpath -L/usr/local/cuda/lib64 -lcudart
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -17,6 +21,7 @@
 #include <vector>
 
 #include "rollout/trainer/scoring.hpp"
+#include "rollout/trainer/synthetic_logits.hpp"
 
 using namespace rollout::train;
 
