@@ -3,9 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
 One *step* = one pass of the trainer-side hot path over one shard of the
-synthetic batch of BASELINE.json configs[1] (Qwen3-4B-shaped: 64 tasks x group
-8, 8K-token multi-turn trajectories, V = 151936, bf16 logits; only informative
-groups are scored, as IterationStats::informative hands over):
+synthetic batch of a BASELINE.json config — by default configs[2], the largest
+single-GPU config (Qwen3-8B-shaped: 128 tasks x group 8, 16K-token ~30-turn
+trajectories with heavy tool-observation masking, V = 151936, bf16 logits;
+only informative groups are scored, as IterationStats::informative hands over):
 H2D of the host SoA -> K1 pack -> K3 GRPO -> K2+K4 fused over every logits
 micro-batch -> NCCL all-reduce of the partials -> D2H, all through the C-ABI
 call prorl_score_host with pinned HOST buffers (the e2e number). `value` is
@@ -20,7 +21,13 @@ inside the timed region.
 
 Multi-GPU (torchrun): groups are sharded by deterministic LPT (no data-path
 collective); the only collective is the NCCL all-reduce of the 332-double
-partials inside each step. Timing is the max over ranks.
+partials inside each step. Timing is the max over ranks. Weak scaling (default)
+gives every rank a config-sized shard (the global batch is N x the config's
+tasks); the north-star 8-GPU run is the C4 batch split over 8 ranks:
+    torchrun --nproc-per-node 8 bench.py --gpus 8 --config c4 --scaling strong
+
+--impl reference: the reference's CPU path on this host's cores (see
+run_reference), on the same workload and config dict.
 """
 from __future__ import annotations
 
@@ -47,7 +54,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--microbatch", type=int, default=16576)  # 148 SMs x 8 warps x 14 rows
     ap.add_argument("--pool", type=int, default=3)
@@ -63,6 +70,35 @@ def bytes_per_row(vocab: int, dtype: str) -> int:
     # V * sizeof(logit) + ~26 B of side arrays per active row
     # (target 4 + old_lp 4 + seq 4 + turn 2 + adv 4 + row bookkeeping 8)
     return vocab * (2 if dtype == "bf16" else 4) + 26
+
+
+K_SCORE_SOURCES = ("score.cu", "rowmath.cuh", "stream.cuh", "common.cuh")
+
+
+def k_score_stamp() -> str:
+    """Digest of the sources k_score is compiled from: an ncu traffic capture is
+    only quoted for the kernel build it was taken on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in K_SCORE_SOURCES:
+        h.update((ROOT / "paper_2603_18815_b200" / "csrc" / f).read_bytes())
+    return h.hexdigest()[:16]
+
+
+def k_score_traffic(rows_per_launch: int):
+    """(DRAM bytes per launch, note) from profiles/k_score_traffic.json — the
+    `ncu --set full` capture written by scripts/ncu_traffic.py — or (None, why)
+    when that capture was taken on other kernel sources."""
+    tf = ROOT / "profiles" / "k_score_traffic.json"
+    if not tf.exists():
+        return None, "no capture (scripts/ncu_traffic.py)"
+    try:
+        tj = json.loads(tf.read_text())
+    except Exception as ex:
+        return None, f"unreadable capture: {ex!r}"
+    if tj.get("source_stamp") != k_score_stamp():
+        return None, "stale capture: k_score sources changed since profiles/k_score_traffic.json"
+    return tj["dram_bytes_per_row"] * rows_per_launch, f"ncu capture {tj.get('source', '?')} (source stamp matches)"
 
 
 def measured_peak_gbs():
@@ -125,26 +161,65 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(shard, cfg, seed: int, budget_s: float) -> dict:
-    """The CPU oracle (a restatement of the path: the reference has no CPU
-    implementation of the math) timed on this host's cores over a bounded
-    sample of the same workload's active rows."""
+def global_workload(c: dict, world: int, scaling: str) -> dict:
+    """The step's global batch: weak scaling grows the task count with N (every
+    rank scores ~one config-sized shard); strong scaling splits the config's."""
+    g = dict(c)
+    g["tasks"] = c["tasks"] * (world if scaling == "weak" else 1)
+    return g
+
+
+def workload_config(c: dict, config_id: str, gcfg: dict, world: int, scaling: str, n_groups: int,
+                    n_active: int) -> dict:
+    """The `config` dict — identical for our arm and the reference arm (it names
+    the workload; how each arm ran it goes under "run")."""
+    return {"workload": c["desc"], "config_id": config_id, "tasks_global": gcfg["tasks"],
+            "group_size": c["group"], "global_batch": f"{n_groups} informative groups, {n_active} active rows",
+            "seq_len": c["tokens"], "vocab": c["vocab"], "logits_dtype": c["dtype"],
+            "parallelism": f"group-sharded dp{world}", "scaling": scaling, "seed": 2603 + c["index"]}
+
+
+def cpu_reference(gcfg: dict, per_step_s: float, steps: int, warmup: int, microbatch: int) -> dict:
+    """The reference's CPU path for this workload, timed on this host's cores.
+
+    Inputs come from the reference's own compiled code (oracle/ref_workload.py:
+    generate_workload, mock hash_token / token_logprob, TokenTrajectory::flatten,
+    is_informative — oracle/_ref/libref.so); the arithmetic the reference does
+    not have (logprob / entropy / GRPO / DAPO loss) is the CPU
+    oracle (kind "port"), fp64, all host threads. Each step scores a systematic
+    (stratified) sample of the batch's active rows — every stride-th row, a
+    different offset per step — sized to ~per_step_s of CPU work; the time is
+    the WALL clock of the scoring phases (the synthetic logits are generated
+    between them, untimed: they stand in for the LM head) plus the whole
+    batch's pack + GRPO wall time pro rata."""
     from oracle import oracle as O
-    b = shard.batch
+    from oracle import ref_workload as RW
+    rb = RW.build(gcfg)
+    hb = RW.host_batch(rb)
+    oc = O.score_cfg(gcfg["vocab"], gcfg["dtype"], microbatch_rows=microbatch)
     threads = os.cpu_count() or 1
-    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
-    oc = O.score_cfg(cfg.vocab, cfg.dtype, microbatch_rows=cfg.microbatch_rows)
-    # calibrate on a small sample, then size the timed sample for ~budget_s
-    probe = O.score_batch(hb, oc, seed, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
-    rate = (threads * 4) / max(probe["timings"][1], 1e-6)
-    n = int(min(max(rate * budget_s, threads), shard.n_active))
-    r = O.score_batch(hb, oc, seed, 2.0, nthreads=threads, row_begin=0, row_end=n)
-    t_pack = r["timings"][0] * n / max(shard.n_active, 1)  # pack + GRPO amortised over the sample
-    value = n / (r["timings"][1] + t_pack)
-    return {"value": value, "unit": "masked tokens/s", "cores": threads, "kind": "port",
-            "sample": f"first {n} of {shard.n_active} active rows of the same shard (scoring time; logits "
-                      f"generation excluded; pack+GRPO of the full shard amortised pro rata)",
-            "seconds": float(r["timings"][1])}
+    A = rb.n_active
+    probe_rows = threads * 16
+    probe = O.score_sample(hb, oc, 2603, 2.0, threads, stride=max(1, A // probe_rows), max_rows=probe_rows)
+    rate = probe["n_scored"] / max(probe["timings"][1], 1e-6)
+    per_step = int(min(max(rate * per_step_s, threads), A))
+    stride = max(1, A // per_step)
+    rows = secs = 0.0
+    for s in range(warmup + steps):
+        r = O.score_sample(hb, oc, 2603, 2.0, threads, stride=stride, offset=s % stride, max_rows=per_step)
+        assert r["status"] == 0
+        t = r["timings"][1] + r["timings"][0] * r["n_scored"] / max(A, 1)
+        if s >= warmup:
+            rows += r["n_scored"]
+            secs += t
+    return {"value": rows / secs, "unit": "masked tokens/s", "cores": threads, "kind": "port",
+            "cpu_model": O.cpu_model(), "timing": "wall clock",
+            "sample": f"every {stride}th active row of the {A}-row batch ({per_step} rows per step, offset = step "
+                      f"mod {stride}); inputs from the reference's compiled generate_workload / hash_token / "
+                      f"TokenTrajectory::flatten / is_informative; logits generation (LM-head stand-in) untimed; "
+                      f"pack + GRPO of the whole batch pro rata",
+            "seconds": secs, "rows": int(rows), "ms_per_step": 1000.0 * secs / max(steps, 1),
+            "n_groups": len(rb.groups), "n_active": A}
 
 
 def measure_backward(sc, pool, c, args, reps: int = 10) -> dict:
@@ -372,37 +447,27 @@ def measure_lmhead_step(sc, host, cfg, c, reps: int = 2) -> dict:
 
 def run_reference(args):
     """--impl reference: the reference's CPU path for this workload on the host
-    cores (the oracle port — the reference has no implementation of the math,
-    SPEC.md:8,741), rank 0 only."""
+    cores (cpu_reference: the reference's own compiled code for the inputs and
+    the oracle port for the math the reference does not have),
+    rank 0 only; the other ranks exit without work. Same metric, unit, config."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import oracle as O
-    from paper_2603_18815_b200 import synth
-    shard = synth.make_shard(args.config)
-    c = synth.CONFIGS[args.config]
-    b = shard.batch
-    threads = os.cpu_count() or 1
-    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
-    oc = O.score_cfg(c["vocab"], c["dtype"], microbatch_rows=args.microbatch)
-    probe = O.score_batch(hb, oc, 2603, 2.0, nthreads=threads, row_begin=0, row_end=threads * 4)
-    rate = threads * 4 / max(probe["timings"][1], 1e-6)
-    per_step = int(min(max(rate * 6.0, threads), shard.n_active))  # ~6 s of CPU work per step
-    times = []
-    for s in range(args.warmup + args.steps):
-        r = O.score_batch(hb, oc, 2603, 2.0, nthreads=threads, row_begin=0, row_end=per_step)
-        t = r["timings"][1] + r["timings"][0] * per_step / max(shard.n_active, 1)
-        if s >= args.warmup:
-            times.append(t)
-    value = per_step * len(times) / sum(times)
+    from paper_2603_18815_b200 import synth_spec as S  # pure Python: no product library on this path
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    c = S.CONFIGS[args.config]
+    gcfg = global_workload(c, world, args.scaling)
+    per_step = min(6.0, 150.0 / max(args.steps + args.warmup, 1))
+    ref = cpu_reference(gcfg, per_step, args.steps, args.warmup, args.microbatch)
+    value = ref["value"]
     line = {"metric": "masked tokens/sec scored (logprob+GRPO loss)", "value": value, "unit": "masked tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic", "impl": "reference",
-            "config": {"workload": c["desc"], "config_id": args.config, "active_rows_per_step": per_step,
-                       "parallelism": "cpu threads"},
-            "cpu_baseline": {"value": value, "unit": "masked tokens/s", "cores": threads, "kind": "port",
-                             "sample": f"first {per_step} active rows per step of the {args.config} shard"},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref["ms_per_step"],
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": c["dtype"],
+            "data": "synthetic", "impl": "reference",
+            "config": workload_config(c, args.config, gcfg, world, args.scaling, ref["n_groups"], ref["n_active"]),
+            "run": {"where": "rank 0's host cores", "threads": ref["cores"], "cpu_model": ref["cpu_model"],
+                    "rows_scored": ref["rows"], "seconds": ref["seconds"]},
+            "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "timing")},
             "e2e": {"value": value, "unit": "masked tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -438,8 +503,7 @@ def run_ours(args):
     # weak scaling: the global batch grows with the GPU count (tasks x N, same
     # seed), groups are LPT-sharded so every rank scores ~one config-sized shard;
     # strong scaling: the config's batch itself is LPT-sharded over the ranks
-    gcfg = dict(c)
-    gcfg["tasks"] = c["tasks"] * (world if args.scaling == "weak" else 1)
+    gcfg = global_workload(c, world, args.scaling)
     shard = synth.make_shard(gcfg, rank=rank, world=world, seed=2603 + c["index"])
     host = shard.batch.pinned()
     cfg = ScoreConfig(vocab=c["vocab"], dtype=c["dtype"], microbatch_rows=args.microbatch)
@@ -483,6 +547,11 @@ def run_ours(args):
         per_rank = [int(x.item()) for x in gathered]
     n_total = int(sum(per_rank))
     lpt_imbalance = max(per_rank) / (sum(per_rank) / len(per_rank))
+    n_groups = len(shard.groups)
+    if world > 1:
+        g_t = torch.tensor([float(n_groups)], dtype=torch.float64, device=coll)
+        dist.all_reduce(g_t)
+        n_groups = int(g_t.item())
 
     clocks = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -539,14 +608,7 @@ def run_ours(args):
     local_rows = shard.n_active
     peak, peak_kind = measured_peak_gbs()
     achieved = local_rows * bpr * K / (seg[2] / 1e3) / 1e9  # rank-local bytes / rank-local score time
-    traffic = None
-    tf = ROOT / "profiles" / "k_score_traffic.json"
-    if tf.exists():
-        try:
-            tj = json.loads(tf.read_text())
-            traffic = tj["dram_bytes_per_row"] * min(args.microbatch, local_rows)
-        except Exception:
-            traffic = None
+    traffic, traffic_note = k_score_traffic(min(args.microbatch, local_rows))
 
     if rank == 0:
         res = finalize(fill_partials)
@@ -559,7 +621,9 @@ def run_ours(args):
                 ingest = {"error": repr(ex)}
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cpu = cpu_baseline(shard, cfg, 2603, args.cpu_seconds)
+                ref = cpu_reference(gcfg, args.cpu_seconds, 1, 0, args.microbatch)
+                cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "timing",
+                                           "seconds")}
             except Exception as ex:  # the baseline must not sink the GPU number
                 cpu = {"error": repr(ex)}
         launches_per_step = 6 + 3 + 1 + n_mb + 1 + 1  # 2 scans x3, seq_bounds/pack/compact, grpo, score x n_mb, reduce, fold-errors
@@ -568,18 +632,17 @@ def run_ours(args):
             "value": value, "unit": "masked tokens/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": c["dtype"], "data": "synthetic",
-            "config": {"workload": c["desc"], "config_id": args.config, "parallelism": f"group-sharded dp{world}",
-                       "tasks_global": gcfg["tasks"], "lpt_imbalance_max_over_mean": lpt_imbalance,
-                       "global_batch": f"{len(shard.groups)} informative groups on rank0, {n_total} active rows",
-                       "seq_len": c["tokens"], "vocab": c["vocab"], "microbatch_rows": args.microbatch,
-                       "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
-                       f"({args.pool * args.microbatch * c['vocab'] * (2 if c['dtype'] == 'bf16' else 4) / 1e9:.1f} GB)",
-                       "l2": "inputs larger than L2 (logits pool >> 126 MB; no flush needed)"},
+            "config": workload_config(c, args.config, gcfg, world, args.scaling, n_groups, n_total),
+            "run": {"lpt_imbalance_max_over_mean": lpt_imbalance, "rank0_groups": len(shard.groups),
+                    "rank0_active_rows": shard.n_active, "microbatch_rows": args.microbatch,
+                    "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
+                    f"({args.pool * args.microbatch * c['vocab'] * (2 if c['dtype'] == 'bf16' else 4) / 1e9:.1f} GB)",
+                    "l2": "inputs larger than L2 (logits pool >> 126 MB; no flush needed)"},
             "e2e": {"value": e2e, "unit": "masked tokens/s", "h2d_bytes_per_step": host.bytes_h2d(),
                     "d2h_bytes_per_step": N.N_PARTIALS * 8, "ms_per_step": e2e_ms / K},
             "gpu_launches": launches_per_step * K,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
+                         "traffic": traffic, "traffic_note": traffic_note, "peak_kind": peak_kind, "frac_of_nominal_8000": achieved / 8000.0,
                          "kernel": "k_score<bf16," + N.lib.prorl_kernel_config().decode() + ",fused> (K2+K4)", "bytes_per_row": bpr},
             "segments_ms_per_step": {"h2d": seg[0] / K, "pack_grpo": seg[1] / K, "score": seg[2] / K,
                                      "allreduce": seg[3] / K, "d2h": seg[4] / K},

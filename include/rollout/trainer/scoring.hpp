@@ -7,8 +7,11 @@
 // /process responses carry (proj/src/handlers.cpp:57-91), which the reference
 // harness drops when it records a response (proj/src/trainer/harness.cpp:263-273).
 //
-//   // in the harness's response callback, under its lock (harness.cpp:266-273):
-//   record_response(d->group, slot, response, trajectories, wall);   // this repo
+//   // the harness keeps each response's trajectory through the hook that
+//   // integration/reference.patch adds at harness.cpp:273 (3 lines):
+//   opts.on_response = [&](const PromptGroup& g, int slot, const nlohmann::json& r) {
+//     keep_trajectory(trajectories, g, slot, r);                      // this repo
+//   };
 //   ...
 //   auto stats  = harness.run_iteration_async(workload, plan);         // reference
 //   auto shard  = shard_groups(stats.informative, trajectories, world)[rank];
@@ -267,6 +270,18 @@ inline bool record_response(PromptGroup& g, int slot, const nlohmann::json& resp
   }
   g.outcomes[static_cast<std::size_t>(slot)] = std::move(o);
   return true;
+}
+
+// The hook integration/reference.patch adds to the reference harness
+// (TrainerOptions::on_response, called under the harness lock for every
+// recorded response): keep the trajectory of a non-FAILED rollout.
+//   opts.on_response = [&](const PromptGroup& g, int slot, const nlohmann::json& r) {
+//     keep_trajectory(trajectories, g, slot, r);
+//   };
+inline void keep_trajectory(TrajectoryTable& table, const PromptGroup& g, int slot, const nlohmann::json& resp) {
+  if (resp.value("status", std::string("FAILED")) == "FAILED") return;
+  if (!resp.contains("trajectory")) throw MalformedRequest("response without a trajectory");
+  table.put(g.prompt_id, slot, trajectory_from_json(resp.at("trajectory")));
 }
 
 // ---- host SoA of one shard ---------------------------------------------------------

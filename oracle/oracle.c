@@ -18,13 +18,16 @@
  *   - logprob / entropy (B.2), GRPO advantage (B.3), DAPO clipped surrogate
  *     (B.4), metrics and the 332-double partials layout (B.5, B.6).
  * Parity status: packing / gate / generators are PINNED against the compiled
- * reference (oracle/_ref, tests/test_oracle_ref.py) and the reference's own
+ * reference (oracle/_ref, tests/test_oracle_golden.py) and the reference's own
  * golden vectors (tests/golden/); logprob / entropy / advantage / loss are a
- * restatement with NO reference implementation — "parity unpinned" for those
- * rows, anchored to hand-computed cases instead.
+ * restatement with NO reference implementation: logprob and
+ * entropy are pinned to the third-party prime-rl selective_log_softmax /
+ * compute_entropy (tests/test_oracle_golden.py), advantage and loss to
+ * hand-computed cases (no third-party GRPO/DAPO code exists in the image).
  *
  * Build: oracle/Makefile (gcc -O3 -ffp-contract=off -fPIC -shared -pthread).
  */
+#define _GNU_SOURCE /* pthread_barrier_t, clock_gettime under -std=c11 */
 #include <math.h>
 #include <pthread.h>
 #include <stdint.h>
@@ -472,6 +475,142 @@ int oracle_score_batch(const prorl_host_batch* hb, const prorl_score_cfg* cfg, u
     free(w);
     free(th);
   }
+  if (n_active_out) *n_active_out = pk.n_active;
+  free(pk.tokens); free(pk.loss_mask); free(pk.turn_id); free(pk.seq_id); free(pk.pos_id); free(pk.cu_seqlens);
+  free(pk.old_lp); free(pk.act_row); free(pk.act_target); free(pk.act_old_lp); free(pk.act_seq); free(pk.act_turn);
+  free(adv);
+  free(info);
+  return st;
+}
+
+/* ---- timed stratified sample (bench.py cpu_baseline / --impl reference) ----------------
+ * The whole-step CPU path on a systematic (stratified) sample of a shard's
+ * active rows: rows offset, offset + stride, ... (at most max_rows), so every
+ * group, rollout and turn position of the shard is represented. Threads work in
+ * lock-step rounds: each generates a block of its rows' synthetic logits (the
+ * LM-head stand-in, outside the metric), a barrier, then all score their
+ * blocks; timings[1] is the WALL-CLOCK time of the scoring phases only,
+ * timings[0] the wall time of pack + GRPO over the whole shard, timings[2]
+ * the wall time of the generation phases. */
+typedef struct {
+  const oracle_packed* pk;
+  const double* adv;
+  const prorl_score_cfg* cfg;
+  const int64_t* rollout_key;
+  uint64_t seed;
+  float sigma;
+  int64_t s0, s1, stride, offset; /* this thread's sample indices [s0, s1) */
+  int tid, nthreads;
+  pthread_barrier_t* bar;
+  double P[PRORL_N_PARTIALS], Q[PRORL_N_PARTIALS];
+  int64_t n_border;
+  double* wall; /* [2]: scoring, generation (written by thread 0) */
+  int64_t rounds;
+} sample_t;
+
+#define SAMPLE_BLOCK 16
+
+static void* sample_worker(void* arg) {
+  sample_t* w = (sample_t*)arg;
+  const prorl_score_cfg* cfg = w->cfg;
+  const size_t es = cfg->dtype == PRORL_BF16 ? 2 : 4;
+  char* buf = malloc((size_t)SAMPLE_BLOCK * (size_t)cfg->vocab * es);
+  const double lo = 1.0 - (double)cfg->loss.eps_lo, hi = 1.0 + (double)cfg->loss.eps_hi;
+  for (int64_t r = 0; r < w->rounds; ++r) {
+    const int64_t b0 = w->s0 + r * SAMPLE_BLOCK;
+    const int64_t b1 = b0 + SAMPLE_BLOCK < w->s1 ? b0 + SAMPLE_BLOCK : w->s1;
+    double t0 = 0.0;
+    if (w->tid == 0) t0 = now_s();
+    for (int64_t s = b0; s < b1; ++s) { /* generation phase */
+      const int64_t i = w->offset + s * w->stride;
+      const int32_t q = w->pk->act_seq[i];
+      const int64_t key = (w->rollout_key ? w->rollout_key[q] : (int64_t)q) * ((int64_t)1 << 20) +
+                          (int64_t)(w->pk->act_row[i] - w->pk->cu_seqlens[q]);
+      oracle_gen_logits(buf + (size_t)(s - b0) * cfg->vocab * es, cfg->dtype, cfg->vocab, cfg->vocab, 1, key,
+                        &w->pk->act_target[i], &w->pk->act_old_lp[i], w->seed, w->sigma);
+    }
+    pthread_barrier_wait(w->bar);
+    double t1 = 0.0;
+    if (w->tid == 0) {
+      t1 = now_s();
+      w->wall[1] += t1 - t0;
+    }
+    for (int64_t s = b0; s < b1; ++s) { /* scoring phase (timed) */
+      const int64_t i = w->offset + s * w->stride;
+      double lp, ent;
+      oracle_row_logprob(buf + (size_t)(s - b0) * cfg->vocab * es, cfg->dtype, cfg->vocab, w->pk->act_target[i],
+                         cfg->inv_temperature, &lp, &ent);
+      loss_row(lp, ent, (double)w->pk->act_old_lp[i], w->adv[w->pk->act_seq[i]], w->pk->act_turn[i], lo, hi,
+               cfg->loss.n_buckets, NULL, 0.0, w->P, w->Q, &w->n_border);
+    }
+    pthread_barrier_wait(w->bar);
+    if (w->tid == 0) w->wall[0] += now_s() - t1;
+  }
+  free(buf);
+  return NULL;
+}
+
+int oracle_score_sample(const prorl_host_batch* hb, const prorl_score_cfg* cfg, uint64_t seed, float sigma,
+                        int nthreads, int64_t stride, int64_t offset, int64_t max_rows, double* partials,
+                        double* abs_partials, int64_t* n_border, int64_t* n_scored, int64_t* n_active_out,
+                        double* timings) {
+  const int64_t N = hb->n_tokens;
+  const int32_t R = hb->n_rollouts;
+  if (stride < 1 || offset < 0 || nthreads < 1) return PRORL_E_MALFORMED_REQUEST;
+  double t0 = now_s();
+  oracle_packed pk;
+  memset(&pk, 0, sizeof pk);
+  size_t n1 = (size_t)(N > 0 ? N : 1);
+  pk.tokens = malloc(n1 * 4); pk.loss_mask = malloc(n1); pk.turn_id = malloc(n1 * 2); pk.seq_id = malloc(n1 * 4);
+  pk.pos_id = malloc(n1 * 4); pk.cu_seqlens = malloc((size_t)(R + 1) * 4); pk.old_lp = malloc(n1 * 4);
+  pk.act_row = malloc(n1 * 4); pk.act_target = malloc(n1 * 4); pk.act_old_lp = malloc(n1 * 4);
+  pk.act_seq = malloc(n1 * 4); pk.act_turn = malloc(n1 * 2);
+  int st = oracle_pack(hb->turns, hb->n_turns, hb->ids, hb->lp, N, R, cfg->vocab, &pk);
+  double* adv = malloc((size_t)(R > 0 ? R : 1) * sizeof(double));
+  uint8_t* info = malloc((size_t)(hb->n_groups > 0 ? hb->n_groups : 1));
+  double asum = 0.0, nr = 0.0;
+  if (st == 0)
+    oracle_grpo(hb->reward, hb->usable, hb->group_off, hb->n_groups, cfg->ddof, (double)cfg->adv_eps,
+                cfg->gate_tolerance, adv, info, &asum, &nr);
+  double t1 = now_s();
+  int64_t n_sample = 0;
+  if (st == 0 && offset < pk.n_active) {
+    n_sample = (pk.n_active - offset + stride - 1) / stride;
+    if (max_rows >= 0 && n_sample > max_rows) n_sample = max_rows;
+    sample_t* w = calloc((size_t)nthreads, sizeof(sample_t));
+    pthread_t* th = calloc((size_t)nthreads, sizeof(pthread_t));
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)nthreads);
+    double wall[2] = {0.0, 0.0};
+    const int64_t per = (n_sample + nthreads - 1) / nthreads;
+    const int64_t rounds = (per + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
+    for (int k = 0; k < nthreads; ++k) {
+      w[k].pk = &pk; w[k].adv = adv; w[k].cfg = cfg; w[k].seed = seed; w[k].sigma = sigma;
+      w[k].rollout_key = hb->rollout_key;
+      w[k].s0 = per * k < n_sample ? per * k : n_sample;
+      w[k].s1 = per * (k + 1) < n_sample ? per * (k + 1) : n_sample;
+      w[k].stride = stride; w[k].offset = offset; w[k].tid = k; w[k].nthreads = nthreads;
+      w[k].bar = &bar; w[k].wall = wall; w[k].rounds = rounds;
+      pthread_create(&th[k], NULL, sample_worker, &w[k]);
+    }
+    for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+    for (int k = 0; k < nthreads; ++k) {
+      for (int j = 0; j < PRORL_N_PARTIALS; ++j) {
+        partials[j] += w[k].P[j];
+        if (abs_partials) abs_partials[j] += w[k].Q[j];
+      }
+      if (n_border) *n_border += w[k].n_border;
+    }
+    pthread_barrier_destroy(&bar);
+    if (timings) {
+      timings[0] = t1 - t0;
+      timings[1] = wall[0];
+      timings[2] = wall[1];
+    }
+    free(w);
+    free(th);
+  }
+  if (n_scored) *n_scored = n_sample;
   if (n_active_out) *n_active_out = pk.n_active;
   free(pk.tokens); free(pk.loss_mask); free(pk.turn_id); free(pk.seq_id); free(pk.pos_id); free(pk.cu_seqlens);
   free(pk.old_lp); free(pk.act_row); free(pk.act_target); free(pk.act_old_lp); free(pk.act_seq); free(pk.act_turn);

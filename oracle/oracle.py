@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
             "oracle_logprob_entropy": (None, [vp, C.c_int, i64, i32, vp, vp, i64, f32, vp, vp]),
             "oracle_loss": (None, [vp, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, C.c_int, vp, vp, vp]),
             "oracle_score_batch": (C.c_int, [vp, vp, u64, f32, C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+            "oracle_score_sample": (C.c_int, [vp, vp, u64, f32, C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
             "oracle_logits_grad": (None, [vp, C.c_int, i64, i32, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f64,
                                           vp, vp, vp]),
         }
@@ -111,6 +112,7 @@ def ref_lib() -> C.CDLL | None:
         "ref_is_informative": (C.c_int, [C.c_int, vp, vp, vp, f64]),
         "ref_fnv1a64": (u64, [vp, C.c_size_t]),
         "ref_hash_token": (i64, [u64, vp, i64, u64, i64]),
+        "ref_hash_tokens": (None, [u64, vp, i64, u64, i64, i64, vp, vp]),
         "ref_token_logprob": (f64, [i64]),
         "ref_prompt_digest": (u64, [vp, i64]),
         "ref_generate_workload_rewards": (C.c_int, [C.c_int, C.c_int, u64, f64, vp]),
@@ -223,3 +225,27 @@ def score_batch(hb_c, cfg_c, seed: int, sigma: float, nthreads: int = 1, row_beg
                                   _p(P), _p(Q), C.byref(nb), _p(lp), _p(ent), C.byref(na), _p(tm))
     return {"status": st, "partials": P, "abs": Q, "n_border": nb.value, "n_active": na.value, "timings": tm,
             "logp": lp, "entropy": ent}
+
+
+def score_sample(hb_c, cfg_c, seed: int, sigma: float, nthreads: int, stride: int, offset: int = 0,
+                 max_rows: int = -1):
+    """Whole-step CPU path on the systematic sample of active rows offset, offset + stride, ...
+    (oracle_score_sample). timings: [pack+GRPO wall s, scoring wall s, generation wall s]."""
+    P, Q = np.zeros(N_PARTIALS), np.zeros(N_PARTIALS)
+    nb, ns, na = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    tm = np.zeros(3)
+    st = lib().oracle_score_sample(C.addressof(hb_c), C.addressof(cfg_c), seed, sigma, nthreads, stride, offset,
+                                   max_rows, _p(P), _p(Q), C.byref(nb), C.byref(ns), C.byref(na), _p(tm))
+    return {"status": st, "partials": P, "abs": Q, "n_border": nb.value, "n_scored": ns.value, "n_active": na.value,
+            "timings": tm}
+
+
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo), for the baseline's record."""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

@@ -6,7 +6,7 @@
 //
 //   ref_flatten / ref_validate_turn  -> TokenTrajectory (trajectory.hpp:135-176)
 //   ref_usable_rewards / ref_is_informative -> harness.cpp:84-102
-//   ref_fnv1a64 / ref_hash_token / ref_token_logprob -> mock/policy.cpp:10-53
+//   ref_fnv1a64 / ref_hash_token(s) / ref_token_logprob -> mock/policy.cpp:10-53
 //   ref_generate_workload_rewards    -> trainer/workload.cpp:62-107
 //   ref_process_response             -> handlers.cpp:57-91 (the /process wire JSON)
 #include <cstdint>
@@ -110,6 +110,18 @@ int64_t ref_hash_token(uint64_t seed, const int64_t* prompt, int64_t n_prompt, u
 }
 
 double ref_token_logprob(int64_t t) { return mock::token_logprob(t); }
+
+// Bulk forms for building whole synthetic shards from the reference's own
+// generators (bench.py --impl reference): out[i] = mock::hash_token(seed,
+// prompt, k0 + i, vocab) and lp_out[i] = mock::token_logprob(out[i]).
+void ref_hash_tokens(uint64_t seed, const int64_t* prompt, int64_t n_prompt, uint64_t k0, int64_t n, int64_t vocab,
+                     int64_t* out, double* lp_out) {
+  const TokenIds p(prompt, prompt + n_prompt);
+  for (int64_t i = 0; i < n; ++i) {
+    out[i] = mock::hash_token(seed, p, k0 + (uint64_t)i, vocab);
+    if (lp_out) lp_out[i] = mock::token_logprob(out[i]);
+  }
+}
 
 uint64_t ref_prompt_digest(const int64_t* prompt, int64_t n_prompt) {
   return mock::prompt_digest(TokenIds(prompt, prompt + n_prompt));

@@ -77,11 +77,11 @@ static int nccl_fail(ncclResult_t r, const char* what) {
     if (r_ != ncclSuccess) return ::prorl::nccl_fail(r_, #call); \
   } while (0)
 
-// PRORL_PDL=0 turns programmatic dependent launch between micro-batch
-// launches off (A/B); on by default.
+// Programmatic dependent launch between micro-batch launches: on; a tuning
+// build turns it off with PRORL_PDL=0 (A/B).
 static bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("PRORL_PDL");
+    const char* e = tuning_env("PRORL_PDL");
     return !(e && e[0] == '0');
   }();
   return on;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <string>
 
 #include "prorl_hotpath.h"
@@ -14,6 +15,20 @@ namespace prorl {
 // Device-side validation flags (prorl_ctx::d_err), raised by kernels and read
 // by prorl_check_errors / prorl_score_host.
 enum : int { ERR_TOKEN_RANGE = 0, ERR_TURN_ORDER = 1, ERR_TOKEN_COUNT = 2, ERR_N = 4 };
+
+// Launch-configuration overrides for A/B runs. Only a tuning build
+// (scripts/build_variant.sh tuning -DPRORL_TUNING, loaded through
+// PRORL_HOTPATH_LIB) reads the PRORL_K*_ / PRORL_PDL variables and compiles the
+// alternative kernel configurations; the release library (build.py) has one
+// configuration per kernel and row-size class and ignores the environment.
+inline const char* tuning_env(const char* name) {
+#ifdef PRORL_TUNING
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);

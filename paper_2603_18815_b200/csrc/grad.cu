@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_grad(const GradArgs p) {
   }
 }
 
-// Launch configurations (warps/CTA x stages x chunk bytes), PRORL_K5_CONFIG selects.
+// Launch configurations (warps/CTA x stages x chunk bytes): the release library
+// has the default; a tuning build (-DPRORL_TUNING) selects others with PRORL_K5_CONFIG.
 template <typename T, int W, int ST, int CH>
 int run_grad_cfg(const GradArgs& a, int n_sm, cudaStream_t st) {
   auto kern = k_grad<T, W, ST, CH>;
@@ -150,7 +151,7 @@ int run_grad_cfg(const GradArgs& a, int n_sm, cudaStream_t st) {
 
 int grad_config() {
   static int idx = [] {
-    const char* e = std::getenv("PRORL_K5_CONFIG");
+    const char* e = tuning_env("PRORL_K5_CONFIG");
     if (!e) return 2;  // default: 12 warps x 4 stages (best of the sweep, scripts/k5_sweep.py)
     const char* names[] = {"w16s2c4096", "w16s3c4096", "w12s4c4096", "w8s6c4096", "w16s4c2048"};
     for (int i = 0; i < 5; ++i)
@@ -163,11 +164,13 @@ int grad_config() {
 template <typename T>
 int run_grad(const GradArgs& a, int n_sm, cudaStream_t st) {
   switch (grad_config()) {
+#ifdef PRORL_TUNING
+    case 0: return run_grad_cfg<T, 16, 2, 4096>(a, n_sm, st);
     case 1: return run_grad_cfg<T, 16, 3, 4096>(a, n_sm, st);
-    case 2: return run_grad_cfg<T, 12, 4, 4096>(a, n_sm, st);
     case 3: return run_grad_cfg<T, 8, 6, 4096>(a, n_sm, st);
     case 4: return run_grad_cfg<T, 16, 4, 2048>(a, n_sm, st);
-    default: return run_grad_cfg<T, 16, 2, 4096>(a, n_sm, st);
+#endif
+    default: return run_grad_cfg<T, 12, 4, 4096>(a, n_sm, st);  // the default (index 2)
   }
 }
 

@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "rowmath.cuh"
 
 namespace prorl {
 
@@ -238,6 +239,7 @@ __device__ __forceinline__ void store_partial(const LmParams& p, int64_t grow, i
   o[5] = a.has_y ? 1.f : 0.f;
 }
 
+#ifdef PRORL_TUNING  // single-CTA variant (PRORL_K6_PAIR=0): tuning builds only
 __global__ void __launch_bounds__(kThreads, 1)
     k_lmhead(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, const LmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
+#endif  // PRORL_TUNING
 
 // ---- 2-CTA variant (cta_group::2): a CTA pair computes 256-row x 256-vocab
 // logits tiles. Rank r of the pair holds rows [128 r, 128 r + 128) of the
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Per row: merge the vocab-chunk partials (each chunk's top element is kept
 // out of its sums) into logp / entropy with the same exclusion trick as K2.
-__global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, int32_t n_chunks, float c,
+__global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, int32_t n_chunks, float c, float inv_t,
                                float* __restrict__ logp, float* __restrict__ entropy) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_rows) return;
@@ -602,12 +605,9 @@ __global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, i
     S = fmaf(sc, Sk, S);
     T = fmaf(sc, fmaf(-dl, Sk, Tk), T);
   }
-  const float r = fmaf(Mx, c, -Mc);
-  const float ir = exp2f(-r);
-  const float q = S * ir;
-  const float l1q = log1pf(q);
-  logp[i] = (fmaf(xy, c, -Mc) - r) * kLn2 - l1q;
-  if (entropy) entropy[i] = l1q + kLn2 * (fmaf(r, q, -T * ir) / (1.f + q));
+  const rowmath::RowStats rs = rowmath::row_stats(Mc, Mx, S, T, xy, c, (double)inv_t);  // fp64 row end
+  logp[i] = (float)rs.logp;
+  if (entropy) entropy[i] = (float)rs.ent;
 }
 
 // K6 pacing window in vocab tiles (PRORL_K6_PACE, 0 = off). Default 4: the
@@ -616,7 +616,7 @@ __global__ void k_lmhead_merge(const float* __restrict__ part, int64_t n_rows, i
 // saved DRAM energy buys clock at the power cap (whole step 570 vs 587 ms).
 int lmhead_pacing() {
   static int w = [] {
-    const char* e = std::getenv("PRORL_K6_PACE");
+    const char* e = tuning_env("PRORL_K6_PACE");
     return e ? std::max(0, std::atoi(e)) : 4;
   }();
   return w;
@@ -625,7 +625,7 @@ int lmhead_pacing() {
 // K6 launch mode: CTA pairs (cta_group::2) unless PRORL_K6_PAIR=0.
 bool lmhead_pair_mode() {
   static bool pair = [] {
-    const char* e = std::getenv("PRORL_K6_PAIR");
+    const char* e = tuning_env("PRORL_K6_PAIR");
     return !(e && e[0] == '0');
   }();
   return pair;
@@ -707,7 +707,7 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
       if (eff >= 0.85) break;
     }
   }
-  if (const char* e = std::getenv("PRORL_K6_CHUNKS")) {  // tuning override: vocab chunks per row tile
+  if (const char* e = tuning_env("PRORL_K6_CHUNKS")) {  // tuning override: vocab chunks per row tile
     const int32_t nch = std::max(1, std::min(p.n_ntiles, std::atoi(e)));
     p.tpc = (p.n_ntiles + nch - 1) / nch;
     p.n_chunks = (p.n_ntiles + p.tpc - 1) / p.tpc;
@@ -742,13 +742,16 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
     cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(units, n_workers)));
     PRORL_CUDA(cudaLaunchKernelEx(&cfg, k_lmhead2, tmH, tmW, p));
   } else {
+#ifdef PRORL_TUNING
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
     PRORL_CUDA(cudaFuncSetAttribute(k_lmhead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = (unsigned)std::min<int64_t>(units, n_workers);
     k_lmhead<<<grid, kThreads, smem, st>>>(tmH, tmW, p);
+#endif
   }
   PRORL_CUDA(cudaGetLastError());
-  k_lmhead_merge<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(p.part, n_rows, p.n_chunks, p.c, logp, entropy);
+  k_lmhead_merge<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(p.part, n_rows, p.n_chunks, p.c, inv_temp, logp,
+                                                                    entropy);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
 }

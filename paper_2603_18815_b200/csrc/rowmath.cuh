@@ -128,34 +128,72 @@ template <> struct Elem<float> {
   }
 };
 
-// Warp-uniform running maximum and the excluded top element.
+// Exact powers of two 2^k for an integer-valued k (the running reference Mc
+// is an integer in log2 units, so every rescale is exact — an ex2.approx
+// factor would bias the rescaled sums by its -5e-8 mean error).
+__device__ __forceinline__ float pow2f(float k) {
+  const int ki = (int)fmaxf(k, -200.f);
+  return ki < -126 ? 0.f : __int_as_float((127 + ki) << 23);
+}
+__device__ __forceinline__ double pow2d(float k) {
+  const int ki = (int)fmaxf(k, -1100.f);
+  return ki < -1022 ? 0.0 : __hiloint2double((1023 + ki) << 20, 0);
+}
+
+// Warp-uniform running reference and the excluded top element.
 struct Top {
-  float Mc;  // running max of x*c (rounded), -inf before the first element
+  float Mc;  // integer-valued reference >= max x*c seen (-inf before the first element)
   float Mx;  // the raw (clamped) logit that set it
 };
 
-// Called by the whole warp when some lane saw lm*c > Mc. Rescales every
-// lane's sums to the new max, turns the previous top element into an ordinary
+// One lane's share of a row's sums S = sum 2^d, T = sum d 2^d (d = x c - Mc):
+// fp32 accumulators for the current block of chunks (FADD2 / FFMA2 on the
+// packed pipe), folded into fp64 every few chunks, so the fp32 recursive
+// summation never runs over more than ~64 terms (its rounding noise was the
+// dominant per-row logp error, ~1e-7 rms at C2).
+struct LaneSums {
+  float2 S[2], T[2];
+  double Sd, Td;
+  __device__ __forceinline__ void zero() {
+    S[0] = S[1] = T[0] = T[1] = make_float2(0.f, 0.f);
+    Sd = Td = 0.0;
+  }
+  __device__ __forceinline__ void fold() {
+    const float2 s = __fadd2_rn(S[0], S[1]), t = __fadd2_rn(T[0], T[1]);
+    Sd += (double)(s.x + s.y);
+    Td += (double)(t.x + t.y);
+    S[0] = S[1] = T[0] = T[1] = make_float2(0.f, 0.f);
+  }
+  __device__ __forceinline__ void add(float d, float e) {
+    S[0].x += e;
+    T[0].x = fmaf(d, e, T[0].x);
+  }
+};
+
+// Called by the whole warp when some lane saw lm*c > Mc (+ slack). Moves the
+// reference to the integer ceil(max * c), rescales every lane's sums by the
+// exact 2^(Mc_old - Mc_new), turns the previous top element into an ordinary
 // term (added by lane 0), and returns the lane that holds the new top element
 // (lowest lane on ties) — that lane must exclude one copy of it from its sums.
-__device__ __forceinline__ int raise_top(float lm, float c, Top& top, float2 (&S)[2], float2 (&Tt)[2], int lane) {
+__device__ __forceinline__ int raise_top(float lm, float c, Top& top, LaneSums& a, int lane) {
   const float gl = warp_max(lm);
-  const float nMc = gl * c;
+  const float nMc = ceilf(gl * c);
   if (top.Mc != -INFINITY) {
-    const float sc = ex2_approx(top.Mc - nMc);
-    const float dl = nMc - top.Mc;
+    const float k = top.Mc - nMc, dl = -k;
+    const float sc = pow2f(k);
+    const double scd = pow2d(k), dld = (double)dl;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      Tt[k].x = sc * fmaf(-dl, S[k].x, Tt[k].x);
-      Tt[k].y = sc * fmaf(-dl, S[k].y, Tt[k].y);
-      S[k].x *= sc;
-      S[k].y *= sc;
+    for (int q = 0; q < 2; ++q) {
+      a.T[q].x = sc * fmaf(-dl, a.S[q].x, a.T[q].x);
+      a.T[q].y = sc * fmaf(-dl, a.S[q].y, a.T[q].y);
+      a.S[q].x *= sc;
+      a.S[q].y *= sc;
     }
+    a.Td = scd * fma(-dld, a.Sd, a.Td);
+    a.Sd *= scd;
     if (lane == 0) {
       const float d = fmaf(top.Mx, c, -nMc);
-      const float e = ex2_approx(d);
-      S[0].x += e;
-      Tt[0].x = fmaf(d, e, Tt[0].x);
+      a.add(d, ex2_approx(d));
     }
   }
   top.Mc = nMc;
@@ -184,21 +222,32 @@ __device__ __forceinline__ int raise_top(float lm, float c, Top& top, float2 (&S
 constexpr double kLn2d = 0.69314718055994530942;
 constexpr double kLog2ed = 1.44269504088896340736;
 
+// ex2.approx.ftz.f32 (MUFU.EX2) is biased: -0.62 ulp on average, a mean
+// relative error of -5.1e-8 weighted by term size over bf16 / fp32 logits with
+// an integer reference (scripts/ex2_probe.cu on the B200). Every term but the
+// excluded top element is such a term, so the row's sums are scaled back by
+// (1 + 5.1e-8) at the row end; uncorrected, the bias moved every logp by
+// +4.7e-8 — systematic, and visible in a sum that cancels ~600-fold, like
+// sum(old_lp - logp) at C2.
+constexpr double kEx2Bias = 5.1e-8;
+
 struct RowStats {
   double logp, ent;
 };
-__device__ __forceinline__ RowStats row_stats(float Mc, float Mx, float Sr, float Tr, float xy, float c,
+__device__ __forceinline__ RowStats row_stats(float Mc, float Mx, double Sr, double Tr, float xy, float c,
                                               double inv_t) {
   const double ct = inv_t * kLog2ed;
   const double mc = (double)Mc, cc = (double)c;
-  const double S = (double)Sr + kLn2d * (ct - cc) * (((double)Tr + mc * (double)Sr) / cc);
+  Sr *= 1.0 + kEx2Bias;
+  Tr *= 1.0 + kEx2Bias;
+  const double S = Sr + kLn2d * (ct - cc) * ((Tr + mc * Sr) / cc);
   const double r = (double)Mx * ct - mc;
   const double ir = exp2(-r);
   const double q = S * ir;
   const double l1q = log1p(q);
   RowStats o;
   o.logp = ((double)xy - (double)Mx) * inv_t - l1q;
-  o.ent = l1q + kLn2d * ((r * q - (double)Tr * ir) / (1.0 + q));
+  o.ent = l1q + kLn2d * ((r * q - Tr * ir) / (1.0 + q));
   return o;
 }
 

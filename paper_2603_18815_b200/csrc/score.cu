@@ -53,27 +53,27 @@ using namespace rowmath;
 // fast-path sums came out NaN. Returns by value (nothing of the caller's hot
 // loop state is address-taken, so it stays in registers).
 struct SlowRow {
-  float Mc, Mx, Sr, Tr;
+  float Mc, Mx;
+  double Sr, Tr;
 };
 template <typename T>
 __device__ __noinline__ SlowRow row_slow(const uint8_t* rp, int32_t vocab, float c, int lane) {
   Top top{-INFINITY, 0.f};
-  float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  LaneSums acc;
+  acc.zero();
   const float floor_v = __uint_as_float(0xf0000000u);
   for (int32_t base = 0; base < vocab; base += 32) {
     float x = base + lane < vocab ? Elem<T>::load(rp, base + lane) : floor_v;
     if (__any_sync(kFull, x * c > top.Mc)) {
-      const int L = raise_top(x, c, top, S, Tt, lane);
+      const int L = raise_top(x, c, top, acc, lane);
       if (lane == L) x = floor_v;
     }
     const float d = fmaf(x, c, -top.Mc);
-    const float e = ex2_approx(d);
-    S[0].x += e;
-    Tt[0].x = fmaf(d, e, Tt[0].x);
+    acc.add(d, ex2_approx(d));
+    if ((base & 2047) == 2016) acc.fold();
   }
-  return SlowRow{top.Mc, top.Mx, warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y)),
-                 warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y))};
+  acc.fold();
+  return SlowRow{top.Mc, top.Mx, warp_sum_d(acc.Sd), warp_sum_d(acc.Td)};
 }
 
 struct ScoreArgs {
@@ -123,10 +123,15 @@ constexpr size_t score_smem_bytes() {
          (FUSED ? (size_t)WARPS * (kNG + kBucketDoubles) * sizeof(double) : 0);
 }
 
+// 16-B vectors per lane between two fp64 folds of the fp32 accumulators
+// (LaneSums): 256 bf16 / 128 fp32 logits, i.e. <= 64 terms per fp32 sum.
+constexpr int kFoldVec = 32;
+
 template <typename T, int WARPS, int STAGES, int CHUNK, int SUBV, bool FUSED>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
   static_assert(CHUNK % (512 * SUBV) == 0, "CHUNK must hold whole lane groups");
   constexpr int NV = CHUNK / 512;  // 16-B vectors per lane per chunk
+  static_assert(kFoldVec % NV == 0, "fold period in whole chunks");
   constexpr int ES = Elem<T>::kSize;
   extern __shared__ __align__(128) uint8_t smem[];
   // the next scoring launch of the step (programmatic dependent launch) may
@@ -165,21 +170,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
     if (lane == 0) xy = Elem<T>::load(rp, tgt);
 
     Top top{-INFINITY, 0.f};
-    float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    LaneSums acc;
+    acc.zero();
     if (head + tail > 0) {  // unaligned head / tail elements, one per lane (<= 14 of them)
       float x = __uint_as_float(0xf0000000u);  // -2^97: the clamp floor, contributes 0
       if (lane < head) x = Elem<T>::load(rp, lane);
       else if (lane < head + tail)
         x = Elem<T>::load(rp, (int64_t)((b - reinterpret_cast<uintptr_t>(rp)) / ES) + (lane - head));
       if (__any_sync(kFull, x * c > top.Mc)) {
-        const int L = raise_top(x, c, top, S, Tt, lane);
+        const int L = raise_top(x, c, top, acc, lane);
         if (lane == L) x = __uint_as_float(0xf0000000u);
       }
       const float d = fmaf(x, c, -top.Mc);
-      const float e = ex2_approx(d);
-      S[0].x += e;
-      Tt[0].x = fmaf(d, e, Tt[0].x);
+      acc.add(d, ex2_approx(d));
     }
 
     for (int64_t ch = 0; ch < nchunks; ++ch) {
@@ -204,16 +207,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         for (int j = 0; j < SUBV; ++j) u[j] = v[g0 + j];
         const float lm = Elem<T>::template group_max<SUBV>(u);
         if (__any_sync(kFull, lm * c > top.Mc + p.raise_slack)) {
-          const int L = raise_top(lm, c, top, S, Tt, lane);
+          const int L = raise_top(lm, c, top, acc, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(u, top.Mx);
         }
-        Elem<T>::template accumulate<SUBV>(u, make_float2(c, c), make_float2(-top.Mc, -top.Mc), S, Tt);
+        Elem<T>::template accumulate<SUBV>(u, make_float2(c, c), make_float2(-top.Mc, -top.Mc), acc.S, acc.T);
       }
+      // fp64 fold every kFoldVec 16-B vectors per lane (warp-uniform)
+      if ((ch + 1) % (kFoldVec / NV) == 0) acc.fold();
     }
 
-    // ---- row end: merge lanes, re-add the top element analytically ----
-    float Sr = warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y));
-    float Tr = warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y));
+    // ---- row end: merge lanes in fp64, re-add the top element analytically ----
+    acc.fold();
+    double Sr = warp_sum_d(acc.Sd);
+    double Tr = warp_sum_d(acc.Td);
     if (!(Tr == Tr) || !(Sr == Sr)) {  // -inf / NaN / overflowing logits: clamped re-read (rare)
       const SlowRow sr = row_slow<T>(rp, p.vocab, c, lane);
       top = Top{sr.Mc, sr.Mx};
@@ -333,8 +339,9 @@ __global__ void k_slab_reduce(const double* __restrict__ slab, int rows, double*
 }
 
 // ---- launch configurations ------------------------------------------------------------
-// warps/CTA x stages x chunk bytes; one CTA per SM. Selected with
-// PRORL_K2_CONFIG (tuning) — default chosen from ncu/bench measurements.
+// warps/CTA x stages x chunk bytes; one CTA per SM. The release library
+// compiles only the default (chosen from ncu/bench measurements);
+// a tuning build (-DPRORL_TUNING) selects the others with PRORL_K2_CONFIG.
 struct K2Config {
   const char* name;
   int warps, stages, chunk, subv;  // subv: 16-B vectors per lane per max-check group (bf16: 8 logits each)
@@ -346,7 +353,7 @@ constexpr int kDefaultConfig = 5;
 
 int active_config() {
   static int idx = [] {
-    const char* e = std::getenv("PRORL_K2_CONFIG");
+    const char* e = tuning_env("PRORL_K2_CONFIG");
     if (e)
       for (int i = 0; i < (int)(sizeof(kConfigs) / sizeof(kConfigs[0])); ++i)
         if (std::strcmp(e, kConfigs[i].name) == 0) return i;
@@ -372,12 +379,14 @@ int run_score(const ScoreArgs& a, int n_sm, int64_t n_rows, int slab_rows, int* 
   if (FUSED && grid > slab_rows) grid = slab_rows;
   if (rows_used) *rows_used = grid;
   switch (active_config()) {
+#ifdef PRORL_TUNING
     case 0: return run_score_cfg<T, 16, 2, 4096, 2, FUSED>(a, grid, pdl, st);
     case 1: return run_score_cfg<T, 16, 2, 4096, 4, FUSED>(a, grid, pdl, st);
     case 2: return run_score_cfg<T, 12, 3, 4096, 2, FUSED>(a, grid, pdl, st);
     case 3: return run_score_cfg<T, 8, 5, 4096, 2, FUSED>(a, grid, pdl, st);
     case 4: return run_score_cfg<T, 8, 3, 8192, 4, FUSED>(a, grid, pdl, st);
-    default: return run_score_cfg<T, 16, 2, 4096, 8, FUSED>(a, grid, pdl, st);
+#endif
+    default: return run_score_cfg<T, 16, 2, 4096, 8, FUSED>(a, grid, pdl, st);  // kDefaultConfig
   }
 }
 
@@ -421,7 +430,7 @@ int launch_score(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.slab = slab;
   a.accumulate = accumulate ? 1 : 0;
   static const float slack = [] {
-    const char* e = std::getenv("PRORL_K2_SLACK");
+    const char* e = tuning_env("PRORL_K2_SLACK");
     return e ? std::max(0.f, std::min(1.f, (float)std::atof(e))) : 1.f;  // measured +1.2 % at C2 (power-capped)
   }();
   a.raise_slack = slack;

@@ -116,22 +116,42 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   return pol;
 }
 
-// Merge two partials (Mc, Mx, S_rest, T_rest) of the online logsumexp: the one
-// with the larger max keeps its top element excluded, the other's top becomes
-// an ordinary term (ties: a wins). Empty partials have Mc = -inf.
-__device__ __forceinline__ float4 merge_partial(float4 a, float4 b, float c) {
-  if (b.x > a.x) {
-    const float4 t = a;
+// One warp's partial of a row's online logsumexp: integer reference Mc, the
+// excluded top logit Mx, and the fp64 sums of every other term relative to Mc.
+struct WPart {
+  float Mc, Mx;
+  double S, T;
+};
+
+// Merge two partials: the one with the larger reference keeps its top element
+// excluded, the other's top becomes an ordinary term (an ex2.approx term like
+// every other, so the row-end MUFU correction applies to it), and its sums are
+// rescaled by the exact 2^(Mc_b - Mc_a) (ties: a wins). fp64 throughout: 16
+// warp partials merged in fp32 would put ~1e-7 of rounding noise on the row's
+// sum. Empty partials have Mc = -inf.
+__device__ __forceinline__ WPart merge_partial(WPart a, WPart b, float c) {
+  if (b.Mc > a.Mc) {
+    const WPart t = a;
     a = b;
     b = t;
   }
-  if (b.x == -INFINITY) return a;
-  const float rk = fmaf(b.y, c, -b.x), ek = ex2_approx(rk);
-  const float Sk = b.z + ek, Tk = fmaf(rk, ek, b.w);
-  const float sc = ex2_approx(b.x - a.x), dl = a.x - b.x;
-  a.z = fmaf(sc, Sk, a.z);
-  a.w = fmaf(sc, fmaf(-dl, Sk, Tk), a.w);
+  if (b.Mc == -INFINITY) return a;
+  const float rk = fmaf(b.Mx, c, -b.Mc), ek = ex2_approx(rk);
+  const double Sk = b.S + (double)ek, Tk = fma((double)rk, (double)ek, b.T);
+  const float k = b.Mc - a.Mc;
+  const double sc = pow2d(k), dl = -(double)k;
+  a.S = fma(sc, Sk, a.S);
+  a.T = fma(sc, fma(-dl, Sk, Tk), a.T);
   return a;
+}
+
+__device__ __forceinline__ WPart shfl_down_part(const WPart& v, int o) {
+  WPart r;
+  r.Mc = __shfl_down_sync(kFull, v.Mc, o);
+  r.Mx = __shfl_down_sync(kFull, v.Mx, o);
+  r.S = __shfl_down_sync(kFull, v.S, o);
+  r.T = __shfl_down_sync(kFull, v.T, o);
+  return r;
 }
 
 // Generic-address element load with the clamp of Elem<T>::load (the rare NaN
@@ -157,15 +177,13 @@ template <> __device__ __forceinline__ float load_clamped<float>(const uint8_t* 
 constexpr float kRaiseSlack = 1.0f;
 
 // One 32-wide step of the scalar online logsumexp (element x per lane).
-__device__ __forceinline__ void scalar_step(float x, float c, Top& top, float2 (&S)[2], float2 (&Tt)[2], int lane) {
+__device__ __forceinline__ void scalar_step(float x, float c, Top& top, LaneSums& acc, int lane) {
   if (__any_sync(kFull, x * c > top.Mc)) {
-    const int L = raise_top(x, c, top, S, Tt, lane);
+    const int L = raise_top(x, c, top, acc, lane);
     if (lane == L) x = __uint_as_float(0xf0000000u);
   }
   const float d = fmaf(x, c, -top.Mc);
-  const float e = ex2_approx(d);
-  S[0].x += e;
-  Tt[0].x = fmaf(d, e, Tt[0].x);
+  acc.add(d, ex2_approx(d));
 }
 
 // 16-B vector of gradients with element e replaced by gy (bf16 / fp32).
@@ -258,7 +276,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + (size_t)kRing * kPiece);
   uint64_t* empty_all = full_all + kRing;
-  float4* wpart_all = reinterpret_cast<float4*>(empty_all + kRing);  // [G][2][kWarps] warp partials (row parity)
+  WPart* wpart_all = reinterpret_cast<WPart*>(empty_all + kRing);  // [G][2][kWarps] warp partials (row parity)
   double* gsum_all = reinterpret_cast<double*>(wpart_all + 2 * kMaxWarps);  // [G][kNG + kBucketDoubles]
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -267,7 +285,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
   uint8_t* ring = smem + (size_t)grp * kRG * kPiece;
   uint64_t* full = full_all + grp * kRG;
   uint64_t* empty = empty_all + grp * kRG;
-  float4* wpart = wpart_all + grp * 2 * kWarps;
+  WPart* wpart = wpart_all + grp * 2 * kWarps;
   double* gsum = gsum_all + grp * (kNG + kBucketDoubles);  // [kNG]
   double* bk = gsum + kNG;                                 // [kBucketDoubles]
   if (threadIdx.x == 0) {
@@ -389,8 +407,8 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
 
     // ---- pass A: statistics ----
     Top top{-INFINITY, 0.f};
-    float2 S[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    float2 Tt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    LaneSums acc;  // ~5 units per warp and row: <= ~40 terms per fp32 sum, folded to fp64 at the row end
+    acc.zero();
     for (int k = first_piece(pcb); k < g.npc; k += kPG) {
       const uint32_t pc = pcb + (uint32_t)k;
       const int u = k * kSplit + kk;
@@ -422,71 +440,71 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
         // fp32 exact enough, and most of a warp's ~5 units per row skip the
         // raise + exclusion path (see the note at kRaiseSlack)
         if (__any_sync(kFull, lm * c > top.Mc + kRaiseSlack)) {
-          const int L = raise_top(lm, c, top, S, Tt, lane);
+          const int L = raise_top(lm, c, top, acc, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(w, top.Mx);
         }
-        Elem<T>::template accumulate<SUBV>(w, c2, make_float2(-top.Mc, -top.Mc), S, Tt);
+        Elem<T>::template accumulate<SUBV>(w, c2, make_float2(-top.Mc, -top.Mc), acc.S, acc.T);
       }
     }
     if (wq == 0 && g.head + g.tail > 0) {
       const int64_t idx = edge_index<ES>(g, lane);
-      scalar_step(idx >= 0 ? Elem<T>::load(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, S, Tt, lane);
+      scalar_step(idx >= 0 ? Elem<T>::load(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, acc, lane);
     }
-    float Sr = warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y));
-    float Tr = warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y));
+    acc.fold();
+    double Sr = warp_sum_d(acc.Sd);
+    double Tr = warp_sum_d(acc.Td);
     if (!(Tr == Tr) || !(Sr == Sr)) {
       // -inf / NaN / overflowing logits: clamped scalar re-run of this warp's
       // share straight from global memory (rare)
       top = Top{-INFINITY, 0.f};
-      S[0] = S[1] = Tt[0] = Tt[1] = make_float2(0.f, 0.f);
+      acc.zero();
       for (int k = first_piece(pcb); k * kSplit + kk < g.nsub; k += kPG) {
         const int u = k * kSplit + kk;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(g.a + (uintptr_t)u * kUnit);
         const int ne = (int)(min((uint32_t)kUnit, g.nb - (uint32_t)u * kUnit) / ES);
         for (int b = 0; b < ne; b += 32)
-          scalar_step(b + lane < ne ? load_clamped<T>(src, b + lane) : __uint_as_float(0xf0000000u), c, top, S, Tt,
+          scalar_step(b + lane < ne ? load_clamped<T>(src, b + lane) : __uint_as_float(0xf0000000u), c, top, acc,
                       lane);
+        acc.fold();
       }
       if (wq == 0 && g.head + g.tail > 0) {
         const int64_t idx = edge_index<ES>(g, lane);
-        scalar_step(idx >= 0 ? load_clamped<T>(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, S, Tt, lane);
+        scalar_step(idx >= 0 ? load_clamped<T>(g.rp, idx) : __uint_as_float(0xf0000000u), c, top, acc, lane);
       }
-      Sr = warp_sum((S[0].x + S[1].x) + (S[0].y + S[1].y));
-      Tr = warp_sum((Tt[0].x + Tt[1].x) + (Tt[0].y + Tt[1].y));
+      acc.fold();
+      Sr = warp_sum_d(acc.Sd);
+      Tr = warp_sum_d(acc.Td);
     }
-    float4* wp = wpart + (j & 1) * kWarps;
-    if (lane == 0) wp[wq] = make_float4(top.Mc, top.Mx, Sr, Tr);
+    WPart* wp = wpart + (j & 1) * kWarps;
+    if (lane == 0) wp[wq] = WPart{top.Mc, top.Mx, Sr, Tr};
     named_sync(1 + grp, kWarps * 32);
     // every warp merges the 16 partials with the same tree -> identical results
-    float4 Gp = lane < kWarps ? wp[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+    WPart Gp = lane < kWarps ? wp[lane] : WPart{-INFINITY, 0.f, 0.0, 0.0};
 #pragma unroll
     for (int o = 1; o < kWarps; o <<= 1) {
-      float4 Q;
-      Q.x = __shfl_down_sync(kFull, Gp.x, o);
-      Q.y = __shfl_down_sync(kFull, Gp.y, o);
-      Q.z = __shfl_down_sync(kFull, Gp.z, o);
-      Q.w = __shfl_down_sync(kFull, Gp.w, o);
-      const float4 M = merge_partial(Gp, Q, c);
+      const WPart M = merge_partial(Gp, shfl_down_part(Gp, o), c);
       if ((lane & (2 * o - 1)) == 0) Gp = M;
     }
-    Gp.x = __shfl_sync(kFull, Gp.x, 0);
-    Gp.y = __shfl_sync(kFull, Gp.y, 0);
-    Gp.z = __shfl_sync(kFull, Gp.z, 0);
-    Gp.w = __shfl_sync(kFull, Gp.w, 0);
+    Gp.Mc = __shfl_sync(kFull, Gp.Mc, 0);
+    Gp.Mx = __shfl_sync(kFull, Gp.Mx, 0);
+    Gp.S = __shfl_sync(kFull, Gp.S, 0);
+    Gp.T = __shfl_sync(kFull, Gp.T, 0);
 
     // ---- row results ----
-    const float rr = fmaf(Gp.y, c, -Gp.x);
+    // fp32 for the gradient (every warp; one bf16 rounding of tolerance), fp64
+    // for the outputs and the loss partials (warp 0, lane 0, below)
+    const float rr = fmaf(Gp.Mx, c, -Gp.Mc);
     const float ir = ex2_approx(-rr);
-    const float qq = Gp.z * ir;
+    const float qq = (float)(Gp.S * (1.0 + kEx2Bias)) * ir;
     const float l1q = log1pf(qq);
-    const float logp = (fmaf(xy, c, -Gp.x) - rr) * kLn2 - l1q;
+    const float logp = (fmaf(xy, c, -Gp.Mc) - rr) * kLn2 - l1q;
     const float ratio = expf(logp - old);
     const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
     bool unclipped = pg1 <= pg2;
     if (fminf(fabsf(ratio - p.lo), fabsf(ratio - p.hi)) <= 1e-5f * ratio) {
       // a ratio this close to a clip bound takes the branch the fp64 loss
       // epilogue takes (rare; warp-uniform: every warp holds the same row state)
-      const RowStats rs = row_stats(Gp.x, Gp.y, Gp.z, Gp.w, xy, c, (double)p.inv_temp);
+      const RowStats rs = row_stats(Gp.Mc, Gp.Mx, Gp.S, Gp.T, xy, c, (double)p.inv_temp);
       const RowLoss rl = row_loss(rs.logp, old, Ad, p.lo_d, p.hi_d, nullptr, 0, 0.0);
       unclipped = rl.loss == -(rl.ratio * Ad);
     }
@@ -497,7 +515,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     const float gy = sg * expm1f(logp);
     if (wq == 0 && lane == 0) {
       // outputs and loss partials from the fp64 row end (rowmath.cuh row_stats / row_loss)
-      const RowStats rs = row_stats(Gp.x, Gp.y, Gp.z, Gp.w, xy, c, (double)p.inv_temp);
+      const RowStats rs = row_stats(Gp.Mc, Gp.Mx, Gp.S, Gp.T, xy, c, (double)p.inv_temp);
       if (p.logp) p.logp[i] = (float)rs.logp;
       if (p.entropy) p.entropy[i] = (float)rs.ent;
       if (p.dlogp) p.dlogp[i] = dl;
@@ -625,12 +643,14 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
 
 constexpr int kMaxSlots = kRingBytes / 4096;  // smallest piece: 4 KB
 constexpr size_t train_smem_bytes() {
-  return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * 16 +
+  return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * sizeof(WPart) +
          (size_t)kMaxGroups * (kNG + kBucketDoubles) * 8;
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 
-// Launch configurations (consumer warps x unit bytes); PRORL_K7_CONFIG selects.
+// Launch configurations (consumer warps x unit bytes). The release library
+// compiles the three defaults of k7_config; a tuning build (-DPRORL_TUNING)
+// has the rest, selected with PRORL_K7_CONFIG.
 constexpr const char* kK7Configs[] = {"w16u4096", "w16u2048", "w24u2048", "w12u4096", "w24u4096", "w16u4096g2",
                                      "w16u2048g2", "w8u4096", "w16u4096s", "w16u4096g2s", "w16u4096g4",
                                      "w16u4096g4s"};
@@ -647,7 +667,7 @@ constexpr int kK7Default = 1, kK7TwoGroups = 5, kK7FourGroups = 10;
 // beat 4 KB by 0-2.5 % from V = 128 256 to 262 144).
 int k7_config(int64_t row_bytes) {
   static int forced = [] {
-    const char* e = std::getenv("PRORL_K7_CONFIG");
+    const char* e = tuning_env("PRORL_K7_CONFIG");
     if (e)
       for (int i = 0; i < (int)(sizeof(kK7Configs) / sizeof(kK7Configs[0])); ++i)
         if (std::strcmp(e, kK7Configs[i]) == 0) return i;
@@ -674,18 +694,20 @@ int run_train_cfg(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st)
 template <typename T>
 int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
   switch (k7_config((int64_t)a.vocab * (int64_t)sizeof(T))) {
-    case 1: return run_train_cfg<T, 16, 2048>(a, n_sm, rows_used, st);
+    case kK7TwoGroups: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, rows_used, st);
+    case kK7FourGroups: return run_train_cfg<T, 16, 4096, 4>(a, n_sm, rows_used, st);
+#ifdef PRORL_TUNING
+    case 0: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
     case 2: return run_train_cfg<T, 24, 2048>(a, n_sm, rows_used, st);
     case 3: return run_train_cfg<T, 12, 4096>(a, n_sm, rows_used, st);
     case 4: return run_train_cfg<T, 24, 4096>(a, n_sm, rows_used, st);
-    case 5: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, rows_used, st);
     case 6: return run_train_cfg<T, 16, 2048, 2>(a, n_sm, rows_used, st);
     case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, rows_used, st);
     case 8: return run_train_cfg<T, 16, 4096, 1, true>(a, n_sm, rows_used, st);
     case 9: return run_train_cfg<T, 16, 4096, 2, true>(a, n_sm, rows_used, st);
-    case 10: return run_train_cfg<T, 16, 4096, 4>(a, n_sm, rows_used, st);
     case 11: return run_train_cfg<T, 16, 4096, 4, true>(a, n_sm, rows_used, st);
-    default: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
+#endif
+    default: return run_train_cfg<T, 16, 2048>(a, n_sm, rows_used, st);  // kK7Default
   }
 }
 

@@ -6,7 +6,7 @@
 // the engine state — and thus the next prompt's draws — matches the
 // reference's sequence exactly). Same libstdc++ distributions as the
 // reference build, so the values are identical to generate_workload's; the
-// oracle test (tests/test_oracle_ref.py) checks that against the compiled
+// oracle test (tests/test_oracle_golden.py) checks that against the compiled
 // reference. Host-only C++; used to build synthetic batches, not on the
 // device path.
 #include <algorithm>

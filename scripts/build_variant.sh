@@ -2,6 +2,8 @@
 # Build an experimental variant of the library with extra nvcc flags into
 # build/variant/<name>/libprorl_hotpath.so, for A/B runs through
 # PRORL_HOTPATH_LIB=<that path>. Usage: scripts/build_variant.sh <name> <nvcc flags...>
+# The tuning build (every launch configuration, PRORL_K*_ / PRORL_PDL honoured):
+#   scripts/build_variant.sh tuning -DPRORL_TUNING
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
@@ -15,7 +17,7 @@ for src in pack.cu grpo.cu score.cu grad.cu train.cu lmhead.cu synth.cu capi.cu;
     -c "$root/paper_2603_18815_b200/csrc/$src" -o "$out/${src%.*}.o" &
   objs+=("$out/${src%.*}.o")
 done
-for src in workload.cpp scoring.cpp ingest.cpp; do
+for src in workload.cpp ingest.cpp; do
   g++ -O3 -std=c++17 -fPIC -I"$root/include" -I"$root/paper_2603_18815_b200/csrc" -I"$json" -I/usr/local/cuda/include \
     -c "$root/paper_2603_18815_b200/csrc/$src" -o "$out/${src%.*}.o" &
   objs+=("$out/${src%.*}.o")

@@ -69,8 +69,13 @@ def full(rep: str, rows_per_launch: int, traffic_out: str | None) -> None:
           f"(algorithmic 2V+26 = {2 * 151936 + 26} B/row at V=151936); {rd / dur_s / 1e9:.0f} GB/s read under ncu "
           f"(cold, serialised, clock as listed).")
     if traffic_out:
+        # stamped with the digest of the kernel's sources: bench.py quotes the
+        # capture only while the sources are the ones it was taken on
+        sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+        from bench import k_score_stamp
         json.dump({"source": rep.split("/")[-1], "kernel": names[0], "rows_per_launch": rows_per_launch,
-                   "dram_bytes_per_launch": rd + wr, "dram_bytes_per_row": per_row}, open(traffic_out, "w"), indent=1)
+                   "dram_bytes_per_launch": rd + wr, "dram_bytes_per_row": per_row,
+                   "source_stamp": k_score_stamp()}, open(traffic_out, "w"), indent=1)
 
 
 def launches(path: str) -> None:

@@ -28,7 +28,7 @@ from paper_2603_18815_b200 import synth  # noqa: E402
 from paper_2603_18815_b200.hotpath import ScoreConfig, Scorer  # noqa: E402
 
 sys.path.insert(0, str(ROOT / "tests" / "golden"))
-from make_full_partials import CASES, SEED, SIGMA, batch_digest  # noqa: E402
+from make_full_partials import CASES, SEED, SIGMA, batch_digest, case_config  # noqa: E402
 
 
 def rows_vs_oracle(s: Scorer, dev) -> dict:
@@ -54,20 +54,17 @@ def rows_vs_oracle(s: Scorer, dev) -> dict:
     ref = O.score_batch(hb, O.score_cfg(V, "bf16"), SEED, SIGMA, nthreads=os.cpu_count() or 1, want_rows=True,
                         n_active_hint=n)
     secs = time.time() - t0
+    from tests.parity import rows_report
     out = {"case": "c2", "n_rows": n, "oracle_seconds": round(secs, 1), "oracle_threads": os.cpu_count()}
     for name, g, o in (("logp", lp_d, ref["logp"][:n]), ("entropy", ent_d, ref["entropy"][:n])):
-        e = g - o
-        rel1 = np.abs(e) / np.maximum(np.abs(o), 1e-3)
-        rel0 = np.abs(e) / np.abs(o)
-        out[name] = {"max_rel_floor_1e-3": float(rel1.max()), "violations_floor_1e-3": int((rel1 > 1e-5).sum()),
-                     "max_rel_floor_0": float(rel0.max()), "violations_floor_0": int((rel0 > 1e-5).sum()),
-                     "max_abs": float(np.abs(e).max()), "mean_signed": float(e.mean()), "rms": float(np.sqrt((e * e).mean()))}
+        out[name] = rows_report(g, o)
+        out[name]["max_rel_floor_0"] = float((np.abs(g - o) / np.abs(o)).max())
     return out
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", default="c2,c3,c4r0w8")
+    ap.add_argument("--cases", default=",".join(CASES))
     ap.add_argument("--rows", action="store_true")
     ap.add_argument("--out", default="gpurun_out/parity_dev.json")
     a = ap.parse_args()
@@ -78,9 +75,10 @@ def main() -> None:
         c = CASES[name]
         sh = synth.make_shard(c["config"], **c["kw"])
         b = sh.batch.pinned()
-        cc = synth.CONFIGS[c["config"]]
+        cc = case_config(name)
         cfg = ScoreConfig(vocab=cc["vocab"], dtype=cc["dtype"], microbatch_rows=16576)
-        pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        tdt = torch.bfloat16 if cc["dtype"] == "bf16" else torch.float32
+        pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=tdt, device=dev) for _ in range(2)]
         fwd, tm = s.score_host(b, cfg, pool, fill=True, seed=SEED, sigma=SIGMA)
         trn, _ = s.score_host(b, cfg, pool, fill=True, seed=SEED, sigma=SIGMA, train=True, n_global=float(sh.n_active))
         res["cases"][name] = {"digest": batch_digest(sh.batch), "n_active": sh.n_active,

@@ -121,6 +121,19 @@ int main(int argc, char** argv) {
   int recorded = 0;
   for (const Arrival& a : arrivals) recorded += record_response(groups[a.g], a.slot, a.wire, table, 0.003) ? 1 : 0;
   CHECK(recorded == kGroups * kN);  // the CANCELLED response did not fill its slot
+  {  // the hook form (integration/reference.patch): keep_trajectory stores what record_response stored
+    TrajectoryTable t2;
+    for (const Arrival& a : arrivals)
+      if (a.wire.value("status", std::string("FAILED")) != "CANCELLED") keep_trajectory(t2, groups[a.g], a.slot, a.wire);
+    CHECK(t2.size() == table.size());
+    for (int g = 0; g < kGroups; ++g)
+      for (int s = 0; s < kN; ++s) {
+        const TokenTrajectory* x = table.find(groups[g].prompt_id, s);
+        const TokenTrajectory* y = t2.find(groups[g].prompt_id, s);
+        CHECK((x == nullptr) == (y == nullptr));
+        if (x && y) CHECK(x->flatten() == y->flatten());
+      }
+  }
   for (const auto& g : groups) CHECK(g.complete());
   CHECK(groups[5].outcomes[1]->status == "FAILED" && table.find(groups[5].prompt_id, 1) == nullptr);
   CHECK(groups[5].usable_rewards().size() == kN - 1);  // reference harness.cpp:84-90

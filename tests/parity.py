@@ -11,6 +11,20 @@ GPU tests, smoke() and scripts/parity_report.py.
     ~0, seven orders of magnitude below the relative bound anywhere else;
   * counts exact, except the clip counters, which may differ by the rows whose
     ratio sits within 1e-5 of a clip bound (counted by the oracle);
+  * small randomized batches (the ragged edge-case tests) whose sums cancel
+    to ~0 by chance may add a random-walk allowance: 6 eps_row * sum|t| /
+    sqrt(n_rows), eps_row = 1e-7 the device's per-row relative accuracy
+    (measured 3.3e-8 rms over all 904 452 C2 rows) — the 6-sigma noise of a
+    sum of n independent per-row errors. The full-size configurations are
+    checked without it;
+  * sum(old_lp - logp) (the k1 KL estimate) is linear in logp and, with the
+    synthetic plant logp = old_lp + U(-0.25, 0.25), cancels 580-4100-fold at
+    full size, so it also sees the device's residual SYSTEMATIC per-row logp
+    error: the MUFU.EX2 bias (-5.1e-8 per term) is corrected at the row end
+    (rowmath.cuh kEx2Bias), which leaves 1.0-1.4e-9 per row (measured on all
+    rows of C2, C3 and the C4 rank-0 shard, where it was 4.7e-8 before). The
+    full-size k1 check adds that bound, SYS_LOGP * n_rows (k1_rows=...), and
+    the parity report records the floor-0 error beside it;
   * sum(A) is exactly 0 in real arithmetic for every informative group (the
     GRPO advantages are centred), so both sides hold only fp64 rounding
     residue there: |g - o| <= 1e-9 * N_rollouts.
@@ -48,7 +62,12 @@ def kind(i: int) -> tuple[str, str]:
     return f"turn_{field}", {"n": "count", "clip": "clip"}.get(field, "sum")
 
 
-def partial_ok(i: int, g: float, o: float, q: float, n_border: int, n_rollouts: float) -> tuple[bool, float]:
+ROW_EPS = 1e-7
+SYS_LOGP = 2e-9
+
+
+def partial_ok(i: int, g: float, o: float, q: float, n_border: int, n_rollouts: float,
+               rw_rows: int | None = None, k1_rows: int | None = None) -> tuple[bool, float]:
     """(within tolerance, relative error |g - o| / |o| or inf/0)."""
     _, rule = kind(i)
     err = abs(g - o)
@@ -59,11 +78,15 @@ def partial_ok(i: int, g: float, o: float, q: float, n_border: int, n_rollouts: 
         return err <= n_border, rel
     if rule == "count":
         return g == o, rel
-    return err <= REL * abs(o) + REASSOC * q, rel
+    allow = REASSOC * q + (6 * ROW_EPS * q / max(rw_rows, 1) ** 0.5 if rw_rows else 0.0)
+    if k1_rows and i == N.P_KL1_SUM:
+        allow += SYS_LOGP * k1_rows
+    return err <= REL * abs(o) + allow, rel
 
 
 def partials_report(got, P, Q, n_border: int) -> dict:
-    """Per quantity: max relative error (floor 0), violations, the rule."""
+    """Per quantity: max relative error (floor 0), violations at floor 0 with no
+    allowance, the rule."""
     got = np.asarray(got, np.float64)
     out: dict = {}
     for i in range(N.N_PARTIALS):
@@ -81,11 +104,11 @@ def partials_report(got, P, Q, n_border: int) -> dict:
     return out
 
 
-def assert_partials_close(got, P, Q, n_border, what=""):
+def assert_partials_close(got, P, Q, n_border, what="", rw_rows: int | None = None, k1_rows: int | None = None):
     got = np.asarray(got, np.float64)
     bad = []
     for i in range(N.N_PARTIALS):
-        ok, rel = partial_ok(i, got[i], P[i], Q[i], n_border, P[N.P_N_ROLLOUTS])
+        ok, rel = partial_ok(i, got[i], P[i], Q[i], n_border, P[N.P_N_ROLLOUTS], rw_rows, k1_rows)
         if not ok:
             bad.append((i, kind(i)[0], got[i], P[i], rel))
     assert not bad, f"{what}: {len(bad)} partials out of tolerance (idx, name, got, oracle, rel): {bad[:6]}"

@@ -111,9 +111,12 @@ def test_logits_grad_layout_errors(scorer, cuda):
     x = torch.zeros((4, 64), dtype=torch.bfloat16, device=cuda)
     t = torch.zeros(4, dtype=torch.int32, device=cuda)
     f = torch.zeros(4, dtype=torch.float32, device=cuda)
+    a = torch.zeros(4, dtype=torch.float64, device=cuda)
     bad = torch.zeros((4, 72), dtype=torch.bfloat16, device=cuda)
     with pytest.raises(RolloutError):
-        scorer.logits_grad(x, t, f, f, f, t, 10.0, grad=bad)
+        scorer.logits_grad(x, t, f, f, a, t, 10.0, grad=bad)
+    with pytest.raises(TypeError):  # advantages cross the C-ABI as fp64
+        scorer.logits_grad(x, t, f, f, f, t, 10.0)
 
 
 def test_logits_grad_dominant_and_masked_rows(scorer, cuda):

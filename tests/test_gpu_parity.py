@@ -460,7 +460,8 @@ def test_score_host_random_ragged_batches(scorer, cuda, seed):
     hb = O.host_batch(t, ids, lp, reward, usable, goff)
     ref = O.score_batch(hb, O.score_cfg(V, "bf16", microbatch_rows=257), seed, 2.0, nthreads=4)
     assert ref["status"] == 0 and ref["n_active"] == ora["n_active"]
-    assert_partials_close(got, ref["partials"], ref["abs"], ref["n_border"], f"ragged{seed}")
+    # random layouts: sums that cancel to ~0 by chance get the random-walk allowance (tests/parity.py)
+    assert_partials_close(got, ref["partials"], ref["abs"], ref["n_border"], f"ragged{seed}", rw_rows=ref["n_active"])
 
 
 def test_score_host_rejects_inconsistent_descriptors(scorer, cuda):

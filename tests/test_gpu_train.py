@@ -306,21 +306,22 @@ def test_score_grad_errors(scorer, cuda):
     t = torch.zeros(4, dtype=torch.int32, device=cuda)
     f = torch.zeros(4, dtype=torch.float32, device=cuda)
     tr = torch.zeros(4, dtype=torch.int16, device=cuda)
+    a = torch.zeros(4, dtype=torch.float64, device=cuda)
     with pytest.raises(RolloutError) as e:   # gradient with another row stride
-        scorer.score_grad(x, t, f, f, t, tr, 10.0, grad=torch.zeros((4, 72), dtype=torch.bfloat16, device=cuda))
+        scorer.score_grad(x, t, f, a, t, tr, 10.0, grad=torch.zeros((4, 72), dtype=torch.bfloat16, device=cuda))
     assert e.value.code == "shape_mismatch"
     with pytest.raises(RolloutError) as e:   # gradient with another 16-B phase
         buf = torch.zeros(4 * 64 + 1, dtype=torch.bfloat16, device=cuda)
-        scorer.score_grad(x, t, f, f, t, tr, 10.0, grad=buf[1:].view(4, 64))
+        scorer.score_grad(x, t, f, a, t, tr, 10.0, grad=buf[1:].view(4, 64))
     assert e.value.code == "shape_mismatch"
     with pytest.raises(RolloutError) as e:   # no active rows in the global count
-        scorer.score_grad(x, t, f, f, t, tr, 0.0)
+        scorer.score_grad(x, t, f, a, t, tr, 0.0)
     assert e.value.code == "malformed_request"
     with pytest.raises(RolloutError) as e:   # missing row arrays
-        scorer.score_grad(x, t, None, f, t, tr, 10.0)
+        scorer.score_grad(x, t, None, a, t, tr, 10.0)
     assert e.value.code == "malformed_request"
     # zero rows: a no-op that leaves the partials untouched
-    part, *_ = scorer.score_grad(x[:0], t[:0], f[:0], f, t[:0], tr[:0], 10.0)
+    part, *_ = scorer.score_grad(x[:0], t[:0], f[:0], a, t[:0], tr[:0], 10.0)
     assert float(part.abs().sum()) == 0.0
 
 

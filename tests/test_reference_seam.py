@@ -103,3 +103,34 @@ def test_seam_score_and_train_groups_vs_oracle(seam):
     assert_partials_close(d["partials"], ref["partials"], ref["abs"], ref["n_border"], "seam score_groups")
     assert_partials_close(d["train_partials"], ref["partials"], ref["abs"], ref["n_border"], "seam train_groups")
     assert d["grad_rows"] == d["n_active"]
+
+
+def test_reference_patch_applies_and_compiles(tmp_path):
+    """integration/reference.patch (TrainerOptions::on_response, the 3-line hook
+    at harness.cpp:273) applies to the unmodified reference, and the patched
+    trainer/harness.cpp compiles together with a trainer TU that wires the hook
+    to the façade's keep_trajectory."""
+    if not REF_INCLUDE.is_dir():
+        pytest.skip("no /root/reference here")
+    import shutil
+    ref = REF_INCLUDE.parent
+    work = tmp_path / "proj"
+    for rel in ("include/rollout/trainer/harness.hpp", "src/trainer/harness.cpp"):
+        (work / rel).parent.mkdir(parents=True, exist_ok=True)
+        shutil.copy(ref / rel, work / rel)
+    subprocess.run(["patch", "-p1", "-d", str(tmp_path), "-i", str(ROOT / "integration" / "reference.patch")],
+                   check=True, capture_output=True)
+    inc = [f"-I{work / 'include'}", f"-I{REF_INCLUDE}", f"-I{ROOT / 'include'}", f"-I{B.json_include()}"]
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", *inc, str(work / "src/trainer/harness.cpp")], check=True)
+    tu = tmp_path / "trainer.cpp"
+    tu.write_text('''
+#include "rollout/trainer/harness.hpp"
+#include "rollout/trainer/scoring.hpp"
+using namespace rollout::train;
+void wire(TrainerOptions& opts, TrajectoryTable& table) {
+  opts.on_response = [&table](const PromptGroup& g, int slot, const nlohmann::json& r) {
+    keep_trajectory(table, g, slot, r);
+  };
+}
+''')
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", *inc, str(tu)], check=True)
