@@ -527,15 +527,30 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     n_mb = (shard.n_active + args.microbatch - 1) // args.microbatch
 
+    def step(fill: bool):
+        """One step; with torch_allreduce the partials are summed over
+        torch.distributed with the library's collective-safe bookkeeping
+        (prorl_fail_partials / prorl_step_status), as prorl_score_host does
+        around its own NCCL all-reduce."""
+        if not torch_allreduce:
+            return sc.score_host(host, cfg, pool, fill=fill, seed=2603)
+        own, tm = 0, np.zeros(5, np.float32)
+        try:
+            p, tm = sc.score_host(host, cfg, pool, fill=fill, seed=2603)
+        except N.RolloutError as ex:
+            own, p = ex.status, np.zeros(N.N_PARTIALS)
+            N.lib.prorl_fail_partials(p.ctypes.data)
+        pt = torch.from_numpy(p).to(coll)
+        dist.all_reduce(pt)
+        p = np.ascontiguousarray(pt.cpu().numpy())
+        N.check(N.lib.prorl_step_status(own, p.ctypes.data))
+        return p, tm
+
     # warm-up: the first call fills the pool with generated logits (LM-head stand-in)
     for w in range(max(args.warmup, 1)):
-        partials, tm = sc.score_host(host, cfg, pool, fill=(w == 0), seed=2603)
+        partials, tm = step(w == 0)
         if w == 0:  # the step whose logits match its targets (reported as "result")
             fill_partials = partials.copy()
-            if torch_allreduce:
-                pt = torch.from_numpy(fill_partials).to(coll)
-                dist.all_reduce(pt)
-                fill_partials = pt.cpu().numpy()
     torch.cuda.synchronize()
 
     # totals over ranks (weak scaling: each rank scores its own groups)
@@ -562,11 +577,7 @@ def run_ours(args):
     clocks.start()
     ev0.record(stream)
     for _ in range(args.steps):
-        partials, tm = sc.score_host(host, cfg, pool, fill=False, seed=2603)
-        if torch_allreduce:
-            pt = torch.from_numpy(partials).to(coll)
-            dist.all_reduce(pt)
-            partials = pt.cpu().numpy()
+        partials, tm = step(False)
         seg += tm
     ev1.record(stream)
     torch.cuda.synchronize()

@@ -369,6 +369,16 @@ int prorl_score_host(prorl_ctx* ctx, const prorl_host_batch* batch, const prorl_
                      const prorl_logits_pool* logits, double* host_partials, float* timings_ms,
                      void* stream);
 
+/* The collective-safe failure bookkeeping prorl_score_host applies, for callers
+ * that reduce the partials themselves (e.g. over torch.distributed):
+ * prorl_fail_partials turns a failed rank's host partials into its
+ * contribution (zeros, partials[PRORL_P_ERR_RANKS] = 1); after the sum,
+ * prorl_step_status(own status, reduced partials) is the step's outcome on
+ * this rank — its own error, PRORL_E_PEER_FAILED if any other rank failed, or
+ * PRORL_OK. Host-only, no ctx. */
+void prorl_fail_partials(double* host_partials);
+int prorl_step_status(int local_status, const double* reduced_host_partials);
+
 #ifdef __cplusplus
 }
 #endif

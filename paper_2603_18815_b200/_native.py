@@ -18,6 +18,9 @@ if os.environ.get("PRORL_HOTPATH_LIB"):  # A/B of an experimental build (scripts
     LIB_PATH = Path(os.environ["PRORL_HOTPATH_LIB"]).resolve()
 
 PRORL_BF16, PRORL_FP32 = 0, 1
+# prorl_status (include/prorl_hotpath.h)
+(PRORL_OK, PRORL_E_MALFORMED_TURN, PRORL_E_INCOMPLETE_GROUP, PRORL_E_MALFORMED_REQUEST) = (0, -1, -2, -3)
+(PRORL_E_CUDA, PRORL_E_NCCL, PRORL_E_SHAPE, PRORL_E_TOKEN_RANGE, PRORL_E_PEER_FAILED) = (-10, -11, -12, -13, -14)
 ROLE_SYSTEM, ROLE_USER, ROLE_ASSISTANT, ROLE_TOOL = 0, 1, 2, 3
 TURN_BUCKETS, N_GLOBAL, N_PER_TURN = 64, 12, 5
 N_PARTIALS = N_GLOBAL + TURN_BUCKETS * N_PER_TURN
@@ -34,7 +37,7 @@ EXPORTS = [
     "prorl_check_errors", "prorl_pack", "prorl_grpo_adv", "prorl_logprob_entropy", "prorl_clipped_loss",
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
     "prorl_gen_logits_keyed", "prorl_row_keys", "prorl_logits_grad", "prorl_score_grad", "prorl_lmhead_logprob", "prorl_ingest_responses", "prorl_ingest_free",
-    "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host",
+    "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host", "prorl_fail_partials", "prorl_step_status",
 ]
 
 vp = C.c_void_p
@@ -119,6 +122,8 @@ def _load() -> C.CDLL:
         "prorl_row_keys": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
         "prorl_synth_rewards": (C.c_int, [i32, i32, u64, f64, vp]),
         "prorl_shard_lpt": (C.c_int, [i32, vp, i32, vp]),
+        "prorl_fail_partials": (None, [vp]),
+        "prorl_step_status": (C.c_int, [C.c_int, vp]),
         "prorl_score_host": (C.c_int, [vp, C.POINTER(HostBatch), C.POINTER(ScoreCfg), C.POINTER(LogitsPool), vp, vp,
                                        vp]),
     }

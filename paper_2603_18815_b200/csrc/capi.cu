@@ -415,13 +415,28 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   cudaStream_t st = S(stream);
   if (cudaSetDevice(c->device) == cudaSuccess && c->partials.ensure(sizeof(double) * PRORL_N_PARTIALS) == cudaSuccess) {
     double* d = c->partials.as<double>();
-    static const double kOne = 1.0;
-    if (cudaMemsetAsync(d, 0, sizeof(double) * PRORL_N_PARTIALS, st) == cudaSuccess &&
-        cudaMemcpyAsync(d + PRORL_P_ERR_RANKS, &kOne, sizeof(double), cudaMemcpyHostToDevice, st) == cudaSuccess)
+    double h[PRORL_N_PARTIALS];
+    prorl_fail_partials(h);
+    if (cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, st) == cudaSuccess)
       nccl().all_reduce(d, d, (size_t)PRORL_N_PARTIALS, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->nccl_comm), st);
     cudaStreamSynchronize(st);
   }
   return fail(rc, msg);
+}
+
+void prorl_fail_partials(double* host_partials) {
+  if (!host_partials) return;
+  std::memset(host_partials, 0, sizeof(double) * PRORL_N_PARTIALS);
+  host_partials[PRORL_P_ERR_RANKS] = 1.0;
+}
+
+int prorl_step_status(int local_status, const double* reduced) {
+  if (local_status != PRORL_OK) return local_status;  // this rank's own failure wins (message already set)
+  if (!reduced) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_step_status: null partials");
+  if (reduced[PRORL_P_ERR_RANKS] > 0.0)
+    return fail(PRORL_E_PEER_FAILED, "peer_failed: " + std::to_string((int)reduced[PRORL_P_ERR_RANKS]) +
+                                         " rank(s) failed this step; the all-reduced partials are void");
+  return PRORL_OK;
 }
 
 namespace {
@@ -654,9 +669,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   PRORL_CUDA(cudaMemcpyAsync(host_partials, partials, sizeof(double) * PRORL_N_PARTIALS, cudaMemcpyDeviceToHost, st));
   PRORL_CUDA(cudaEventRecord(c->ev[5], st));
   PRORL_TRY(prorl_check_errors(c, stream));
-  if (host_partials[PRORL_P_ERR_RANKS] > 0.0)
-    return fail(PRORL_E_PEER_FAILED, "peer_failed: " + std::to_string((int)host_partials[PRORL_P_ERR_RANKS]) +
-                                         " rank(s) failed this step; the all-reduced partials are void");
+  PRORL_TRY(prorl_step_status(PRORL_OK, host_partials));
   if (timings_ms) {
     for (int k = 0; k < 5; ++k) PRORL_CUDA(cudaEventElapsedTime(&timings_ms[k], c->ev[k], c->ev[k + 1]));
   }

@@ -83,3 +83,51 @@ def test_lpt_balances_skewed_groups():
         owner = shard_lpt(load, world)
         per = np.bincount(owner, weights=load, minlength=world)
         assert per.max() / per.mean() < 1.02
+
+
+def _fail_worker(rank, world, port, failing, out):
+    """One step's collective-safe failure bookkeeping (prorl_fail_partials /
+    prorl_step_status — what prorl_score_host does around its NCCL all-reduce)
+    with the partials reduced over gloo: ranks in `failing` contribute the
+    failure record, every rank decides its outcome from the reduced vector."""
+    import ctypes as C
+    from paper_2603_18815_b200 import _native as N
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shard = synth.make_shard(CFG, rank=rank, world=world, seed=5)
+    p = _score(shard)
+    own = N.PRORL_E_SHAPE if rank in failing else 0
+    if own:
+        N.lib.prorl_fail_partials(p.ctypes.data)
+    t = torch.from_numpy(p)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    red = np.ascontiguousarray(t.numpy())
+    st = N.lib.prorl_step_status(own, red.ctypes.data)
+    msg = N.lib.prorl_last_error().decode() if st else ""
+    out.put((rank, st, msg, float(red[N.P_ERR_RANKS])))
+    dist.destroy_process_group()
+    del C
+
+
+@pytest.mark.parametrize("failing", [(), (1,), (0, 1)])
+def test_collective_safe_failure_world2(failing):
+    from paper_2603_18815_b200 import _native as N
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, world, port, failing, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, st, msg, err_ranks in res:
+        assert err_ranks == len(failing)
+        if rank in failing:
+            assert st == N.PRORL_E_SHAPE                  # its own error wins
+        elif failing:
+            assert st == N.PRORL_E_PEER_FAILED and "peer_failed" in msg
+        else:
+            assert st == 0
