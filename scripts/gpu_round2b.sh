@@ -1,0 +1,17 @@
+# Round-2 GPU pass: smoke, GPU suite, device parity, bench (ours + reference arm), ncu traffic + launch list.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+tail -2 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -rf > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -15 gpurun_out/pytest_gpu.log
+timeout 1200 python scripts/parity_dev.py --rows > gpurun_out/parity_dev.log 2>&1; echo parity rc=$?
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c3.log 2>&1; echo bench rc=$?
+tail -c 1500 gpurun_out/bench_c3.log
+timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref rc=$?
+tail -c 1500 gpurun_out/bench_ref.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score -s 3 -c 1 -o gpurun_out/prof_k_score_r02 \
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-backward > gpurun_out/prof_k_score_r02.log 2>&1; echo ncu rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-backward > gpurun_out/launches_r02.log 2>&1; echo launches rc=$?
+ls -la gpurun_out
