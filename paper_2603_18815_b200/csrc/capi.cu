@@ -180,7 +180,7 @@ int prorl_ctx_destroy(prorl_ctx* c) {
                   &c->h_reward, &c->h_usable, &c->h_goff, &c->p_tokens, &c->p_mask, &c->p_turn, &c->p_seq,
                   &c->p_pos, &c->p_cu, &c->p_oldlp, &c->a_row, &c->a_target, &c->a_oldlp, &c->a_seq, &c->a_turn,
                   &c->a_nact, &c->adv, &c->informative, &c->partials, &c->logp, &c->entropy, &c->h_rkey,
-                  &c->row_keys, &c->lm_part, &c->lm_pace})
+                  &c->row_keys, &c->lm_part, &c->lm_pace, &c->k7rows})
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);

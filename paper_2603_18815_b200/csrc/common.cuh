@@ -113,6 +113,7 @@ struct prorl_ctx {
   prorl::DevBuf p_tokens, p_mask, p_turn, p_seq, p_pos, p_cu, p_oldlp;
   prorl::DevBuf a_row, a_target, a_oldlp, a_seq, a_turn, a_nact;
   prorl::DevBuf adv, informative, partials, logp, entropy, h_rkey, row_keys, lm_part, lm_pace;
+  prorl::DevBuf k7rows;  // K7 row-end handoff (per-row fp64 warp partials), see train.cu k_train_rows
   void* nccl_comm = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0;
   cudaEvent_t ev[8] = {};
@@ -196,6 +197,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Non-blocking probe of the phase with `parity` (mbarrier.test_wait).
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)

@@ -175,13 +175,15 @@ struct LaneSums {
 // exact 2^(Mc_old - Mc_new), turns the previous top element into an ordinary
 // term (added by lane 0), and returns the lane that holds the new top element
 // (lowest lane on ties) — that lane must exclude one copy of it from its sums.
+// kFolded = false: the caller has not folded into the fp64 sums yet (they are
+// still zero), so only the fp32 ones need rescaling.
+template <bool kFolded = true>
 __device__ __forceinline__ int raise_top(float lm, float c, Top& top, LaneSums& a, int lane) {
   const float gl = warp_max(lm);
   const float nMc = ceilf(gl * c);
   if (top.Mc != -INFINITY) {
     const float k = top.Mc - nMc, dl = -k;
     const float sc = pow2f(k);
-    const double scd = pow2d(k), dld = (double)dl;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       a.T[q].x = sc * fmaf(-dl, a.S[q].x, a.T[q].x);
@@ -189,8 +191,11 @@ __device__ __forceinline__ int raise_top(float lm, float c, Top& top, LaneSums& 
       a.S[q].x *= sc;
       a.S[q].y *= sc;
     }
-    a.Td = scd * fma(-dld, a.Sd, a.Td);
-    a.Sd *= scd;
+    if constexpr (kFolded) {
+      const double scd = pow2d(k), dld = (double)dl;
+      a.Td = scd * fma(-dld, a.Sd, a.Td);
+      a.Sd *= scd;
+    }
     if (lane == 0) {
       const float d = fmaf(top.Mx, c, -nMc);
       a.add(d, ex2_approx(d));

@@ -78,8 +78,8 @@ struct TrainArgs {
   float* logp;
   float* entropy;
   float* dlogp;
-  double* slab;  // [gridDim.x][PRORL_N_PARTIALS]
-  int accumulate;
+  void* parts;   // [n_rows][kWarps] WPart: each row's fp64 warp partials, for k_train_rows
+  float* xy;     // [n_rows] the rows' target logits (K7 may overwrite them in place)
 };
 
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
@@ -145,13 +145,66 @@ __device__ __forceinline__ WPart merge_partial(WPart a, WPart b, float c) {
   return a;
 }
 
-__device__ __forceinline__ WPart shfl_down_part(const WPart& v, int o) {
-  WPart r;
-  r.Mc = __shfl_down_sync(kFull, v.Mc, o);
-  r.Mx = __shfl_down_sync(kFull, v.Mx, o);
-  r.S = __shfl_down_sync(kFull, v.S, o);
-  r.T = __shfl_down_sync(kFull, v.T, o);
-  return r;
+// One row's contribution to the loss partials (k_train_rows).
+__device__ __forceinline__ void add_row(const RowStats& rs, const RowLoss& rl, float old, int k, double* gsum,
+                                        double* bk) {
+  gsum[0] += rl.loss;
+  gsum[1] += 1.0;
+  gsum[2] += rs.ent;
+  gsum[3] += rs.logp;
+  gsum[4] += rl.ratio;
+  gsum[5] += rl.clip_lo;
+  gsum[6] += rl.clip_hi;
+  gsum[7] += (double)old - rs.logp;
+  gsum[10] += rl.kl;
+  double* b = bk + k * PRORL_N_PER_TURN;
+  b[0] += 1.0;
+  b[1] += rl.loss;
+  b[2] += rs.ent;
+  b[3] += rs.logp;
+  b[4] += rl.clip_lo + rl.clip_hi;
+}
+
+// The merged row state the gradient needs, fp32 (one bf16 rounding of
+// tolerance): every consumer warp merges the warp partials with the same
+// shuffle tree (exact 2^k rescales), so all warps hold identical values.
+struct PartF {
+  float Mc, Mx, S, T;
+};
+__device__ __forceinline__ PartF merge_partial_f(PartF a, PartF b, float c) {
+  if (b.Mc > a.Mc) {
+    const PartF t = a;
+    a = b;
+    b = t;
+  }
+  if (b.Mc == -INFINITY) return a;
+  const float rk = fmaf(b.Mx, c, -b.Mc), ek = ex2_approx(rk);
+  const float Sk = b.S + ek, Tk = fmaf(rk, ek, b.T);
+  const float k = b.Mc - a.Mc;
+  const float sc = pow2f(k);
+  a.S = fmaf(sc, Sk, a.S);
+  a.T = fmaf(sc, fmaf(k, Sk, Tk), a.T);
+  return a;
+}
+
+// The fp64 merge of a row's warp partials, in warp order (the epilogue warp,
+// and a consumer warp deciding a clip-bound row): deterministic.
+template <int K>
+__device__ __noinline__ WPart merge_parts_f64(const WPart* parts, float c) {
+  WPart m = parts[0];
+  for (int k = 1; k < K; ++k) m = merge_partial(m, parts[k], c);
+  return m;
+}
+
+// fp64 decision of the DAPO branch for a row whose fp32 ratio sits within
+// 1e-5 of a clip bound (rare): the branch the fp64 loss epilogue takes.
+template <int K>
+__device__ __noinline__ bool unclipped_f64(const WPart* parts, float xy, float c, double inv_t, float old, double A,
+                                           double lo, double hi) {
+  const WPart m = merge_parts_f64<K>(parts, c);
+  const RowStats rs = row_stats(m.Mc, m.Mx, m.S, m.T, xy, c, inv_t);
+  const RowLoss rl = row_loss(rs.logp, old, A, lo, hi, nullptr, 0, 0.0);
+  return rl.loss == -(rl.ratio * A);
 }
 
 // Generic-address element load with the clamp of Elem<T>::load (the rare NaN
@@ -253,7 +306,7 @@ __device__ __forceinline__ int64_t edge_index(const RowGeo& g, int l) {
 // warp's next piece there), exactly like K2's per-warp ring; no cross-warp
 // mbarrier hand-off remains.
 template <typename T, int SUBV, int W, int UNIT, int G, bool SELF>
-__global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const TrainArgs p) {
+__global__ void __launch_bounds__((W + (SELF ? 0 : 1)) * 32, 1) k_train(const TrainArgs p) {
   constexpr int ES = Elem<T>::kSize;
   constexpr int PB = SELF ? UNIT : kProducerPiece;  // bytes per ring slot / bulk copy
   constexpr int kRing = kRingBytes / PB;     // ring slots per CTA
@@ -277,17 +330,17 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
   uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + (size_t)kRing * kPiece);
   uint64_t* empty_all = full_all + kRing;
   WPart* wpart_all = reinterpret_cast<WPart*>(empty_all + kRing);  // [G][2][kWarps] warp partials (row parity)
-  double* gsum_all = reinterpret_cast<double*>(wpart_all + 2 * kMaxWarps);  // [G][kNG + kBucketDoubles]
+  // warps: W consumers, then (unless SELF) one producer warp whose lane g feeds row group g
+  constexpr int kProdWarp = W;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = warp < W ? warp / kWarps : warp - W;  // row group (consumers) / fed group (producers)
+  const int grp = warp < W ? warp / kWarps : (warp == kProdWarp && !SELF ? lane : 0);  // row group (consumers) / fed group (producer lane)
   const int wq = warp < W ? warp % kWarps : 0;          // warp index inside its group
   uint8_t* ring = smem + (size_t)grp * kRG * kPiece;
   uint64_t* full = full_all + grp * kRG;
   uint64_t* empty = empty_all + grp * kRG;
   WPart* wpart = wpart_all + grp * 2 * kWarps;
-  double* gsum = gsum_all + grp * (kNG + kBucketDoubles);  // [kNG]
-  double* bk = gsum + kNG;                                 // [kBucketDoubles]
+  WPart* parts_g = static_cast<WPart*>(p.parts);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
       mbar_init(&full_all[s], 1);
@@ -295,31 +348,60 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     }
     fence_mbar_init();
   }
-  for (int t = threadIdx.x; t < G * (kNG + kBucketDoubles); t += blockDim.x) gsum_all[t] = 0.0;
   __syncthreads();
 
-  if (!SELF && warp >= W) {
-    // ===== producer: pass A (HBM, keep in L2) then pass B (L2) of each row =====
-    if (lane == 0 && grp < G) {
-      const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
-      uint32_t pc = 0;
-      for (int64_t i = blockIdx.x + (int64_t)grp * gridDim.x; i < p.n_rows; i += (int64_t)G * gridDim.x) {
-        const RowGeo g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
-        const int fh = max(0, g.npc - kRG);  // pieces [fh, npc) stay in the ring for pass B
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int k = 0; k < (pass == 0 ? g.npc : fh); ++k, ++pc) {
-            const int s = (int)(pc % kRG);
-            mbar_wait_t(&empty[s], ((pc / kRG) & 1) ^ 1);
-            const uint32_t bytes = min((uint32_t)kPiece, g.nb - (uint32_t)k * kPiece);
-            fence_proxy_async_smem();  // the consumers' generic reads of this slot before the async-proxy refill
-            mbar_arrive_expect_tx(&full[s], bytes);
-            tma_load_1d(ring + (size_t)s * kPiece, reinterpret_cast<const void*>(g.a + (uintptr_t)k * kPiece), bytes,
-                        &full[s], pass == 0 && k < fh ? pol_a : pol_b);
-          }
+  if (!SELF && warp == kProdWarp) {
+    // ===== producer: pass A (HBM, keep in L2) then pass B (L2) of each row; lane g feeds group g =====
+    // The G lanes stay converged: every iteration each polls its next ring
+    // slot (non-blocking test_wait) and issues the piece when the slot is free,
+    // so no group's refill waits behind another group's (a divergent blocking
+    // wait per lane serialised them).
+    const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
+    uint32_t pc = 0;
+    int64_t i = blockIdx.x + (int64_t)lane * gridDim.x;
+    RowGeo g{};
+    int fh = 0, pass = 0, k = 0;
+    auto settle = [&]() -> bool {  // move (row, pass, k) to the next piece to issue; false when done
+      for (;;) {
+        if (i >= p.n_rows) return false;
+        if (k < (pass == 0 ? g.npc : fh)) return true;
+        if (pass == 0) {
+          pass = 1;
+          k = 0;
+          continue;
+        }
+        i += (int64_t)G * gridDim.x;
+        if (i >= p.n_rows) return false;
+        g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
+        fh = max(0, g.npc - kRG);  // pieces [fh, npc) stay in the ring for pass B
+        pass = 0;
+        k = 0;
+      }
+    };
+    if (lane < G && i < p.n_rows) {
+      g = row_geo<ES, kUnit, PB>(p, p.rows ? (int64_t)p.rows[i] : i);
+      fh = max(0, g.npc - kRG);
+    }
+    bool live = lane < G && settle();
+    uint32_t idle = 0;
+    while (__any_sync(kFull, live)) {
+      if (live) {
+        const int s = (int)(pc % kRG);
+        if (mbar_test_wait(&empty[s], ((pc / kRG) & 1) ^ 1)) {
+          const uint32_t bytes = min((uint32_t)kPiece, g.nb - (uint32_t)k * kPiece);
+          fence_proxy_async_smem();  // the consumers' generic reads of this slot before the async-proxy refill
+          mbar_arrive_expect_tx(&full[s], bytes);
+          tma_load_1d(ring + (size_t)s * kPiece, reinterpret_cast<const void*>(g.a + (uintptr_t)k * kPiece), bytes,
+                      &full[s], pass == 0 && k < fh ? pol_a : pol_b);
+          ++pc;
+          ++k;
+          live = settle();
+          idle = 0;
+        } else if (++idle > (1u << 26)) {
+          __trap();  // a slot never freed: protocol bug (the consumers' waits trap after ~4 s too)
         }
       }
     }
-    __syncwarp();
     return;
   }
 
@@ -440,7 +522,7 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
         // fp32 exact enough, and most of a warp's ~5 units per row skip the
         // raise + exclusion path (see the note at kRaiseSlack)
         if (__any_sync(kFull, lm * c > top.Mc + kRaiseSlack)) {
-          const int L = raise_top(lm, c, top, acc, lane);
+          const int L = raise_top<false>(lm, c, top, acc, lane);  // no fp64 fold before the row end
           if (lane == L) Elem<T>::template mask_first<SUBV>(w, top.Mx);
         }
         Elem<T>::template accumulate<SUBV>(w, c2, make_float2(-top.Mc, -top.Mc), acc.S, acc.T);
@@ -478,66 +560,51 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     WPart* wp = wpart + (j & 1) * kWarps;
     if (lane == 0) wp[wq] = WPart{top.Mc, top.Mx, Sr, Tr};
     named_sync(1 + grp, kWarps * 32);
-    // every warp merges the 16 partials with the same tree -> identical results
-    WPart Gp = lane < kWarps ? wp[lane] : WPart{-INFINITY, 0.f, 0.0, 0.0};
+    // warp 0 hands the row's fp64 warp partials (and its target logit, which pass
+    // B may overwrite in place) to k_train_rows, which finishes the row in fp64
+    // off this kernel's critical path
+    if (wq == 0) {
+      if (lane < kWarps) parts_g[i * kWarps + lane] = wp[lane];
+      if (lane == 0) p.xy[i] = xy;
+    }
+    // every warp merges them in fp32 with the same tree -> identical results
+    PartF Gp = lane < kWarps ? PartF{wp[lane].Mc, wp[lane].Mx, (float)wp[lane].S, (float)wp[lane].T}
+                             : PartF{-INFINITY, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int o = 1; o < kWarps; o <<= 1) {
-      const WPart M = merge_partial(Gp, shfl_down_part(Gp, o), c);
+      PartF Q;
+      Q.Mc = __shfl_down_sync(kFull, Gp.Mc, o);
+      Q.Mx = __shfl_down_sync(kFull, Gp.Mx, o);
+      Q.S = __shfl_down_sync(kFull, Gp.S, o);
+      Q.T = __shfl_down_sync(kFull, Gp.T, o);
+      const PartF M = merge_partial_f(Gp, Q, c);
       if ((lane & (2 * o - 1)) == 0) Gp = M;
     }
     Gp.Mc = __shfl_sync(kFull, Gp.Mc, 0);
     Gp.Mx = __shfl_sync(kFull, Gp.Mx, 0);
     Gp.S = __shfl_sync(kFull, Gp.S, 0);
-    Gp.T = __shfl_sync(kFull, Gp.T, 0);
 
     // ---- row results ----
     // fp32 for the gradient (every warp; one bf16 rounding of tolerance), fp64
     // for the outputs and the loss partials (warp 0, lane 0, below)
     const float rr = fmaf(Gp.Mx, c, -Gp.Mc);
     const float ir = ex2_approx(-rr);
-    const float qq = (float)(Gp.S * (1.0 + kEx2Bias)) * ir;
+    const float qq = Gp.S * ir;
     const float l1q = log1pf(qq);
     const float logp = (fmaf(xy, c, -Gp.Mc) - rr) * kLn2 - l1q;
     const float ratio = expf(logp - old);
     const float pg1 = ratio * A, pg2 = fminf(fmaxf(ratio, p.lo), p.hi) * A;
     bool unclipped = pg1 <= pg2;
-    if (fminf(fabsf(ratio - p.lo), fabsf(ratio - p.hi)) <= 1e-5f * ratio) {
+    if (fminf(fabsf(ratio - p.lo), fabsf(ratio - p.hi)) <= 1e-5f * ratio)
       // a ratio this close to a clip bound takes the branch the fp64 loss
-      // epilogue takes (rare; warp-uniform: every warp holds the same row state)
-      const RowStats rs = row_stats(Gp.Mc, Gp.Mx, Gp.S, Gp.T, xy, c, (double)p.inv_temp);
-      const RowLoss rl = row_loss(rs.logp, old, Ad, p.lo_d, p.hi_d, nullptr, 0, 0.0);
-      unclipped = rl.loss == -(rl.ratio * Ad);
-    }
+      // epilogue takes (rare; warp-uniform: every warp reads the same partials)
+      unclipped = unclipped_f64<kWarps>(wp, xy, c, (double)p.inv_temp, old, Ad, p.lo_d, p.hi_d);
     float dl = unclipped ? -A * ratio * p.inv_n : 0.f;  // dL/dlogp
     if (p.ref_lp) dl = fmaf(p.kl_coef * p.inv_n, -expm1f(ref - logp), dl);
     const float sg = -dl * p.inv_temp;  // grad_v = sg p_v (v != y), grad_y = sg expm1(logp) = -sg (1 - p_y)
     const float l2 = fmaf(xy, c, -logp * kLog2e);
     const float gy = sg * expm1f(logp);
-    if (wq == 0 && lane == 0) {
-      // outputs and loss partials from the fp64 row end (rowmath.cuh row_stats / row_loss)
-      const RowStats rs = row_stats(Gp.Mc, Gp.Mx, Gp.S, Gp.T, xy, c, (double)p.inv_temp);
-      if (p.logp) p.logp[i] = (float)rs.logp;
-      if (p.entropy) p.entropy[i] = (float)rs.ent;
-      if (p.dlogp) p.dlogp[i] = dl;
-      int k = p.row_turn[i];
-      k = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
-      const RowLoss rl = row_loss(rs.logp, old, Ad, p.lo_d, p.hi_d, p.ref_lp, i, (double)p.kl_coef);
-      gsum[0] += rl.loss;
-      gsum[1] += 1.0;
-      gsum[2] += rs.ent;
-      gsum[3] += rs.logp;
-      gsum[4] += rl.ratio;
-      gsum[5] += rl.clip_lo;
-      gsum[6] += rl.clip_hi;
-      gsum[7] += (double)old - rs.logp;
-      gsum[10] += rl.kl;
-      double* b = bk + k * PRORL_N_PER_TURN;
-      b[0] += 1.0;
-      b[1] += rl.loss;
-      b[2] += rs.ent;
-      b[3] += rs.logp;
-      b[4] += rl.clip_lo + rl.clip_hi;
-    }
+    if (wq == 0 && lane == 0 && p.dlogp) p.dlogp[i] = dl;
 
     // ---- pass B: gradient ----
     const bool zero = (sg == 0.f);
@@ -624,27 +691,11 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : G)) * 32, 1) k_train(const Tr
     }
     pcb += (uint32_t)(g.npc + fh);
   }
-
-  // ---- slab row of this CTA: the groups' sums in fixed order ----
-  named_sync(1 + G, W * 32);
-  if (warp == 0) {
-    for (int t = lane; t < PRORL_N_PARTIALS; t += 32) {
-      double v = 0.0;
-      for (int q = 0; q < G; ++q) {
-        const double* gs = gsum_all + q * (kNG + kBucketDoubles);
-        if (t < kNG) v += gs[t];
-        else if (t >= PRORL_N_GLOBAL) v += gs[kNG + t - PRORL_N_GLOBAL];
-      }
-      double* d = p.slab + (size_t)blockIdx.x * PRORL_N_PARTIALS + t;
-      *d = p.accumulate ? *d + v : v;
-    }
-  }
 }
 
 constexpr int kMaxSlots = kRingBytes / 4096;  // smallest piece: 4 KB
 constexpr size_t train_smem_bytes() {
-  return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * sizeof(WPart) +
-         (size_t)kMaxGroups * (kNG + kBucketDoubles) * 8;
+  return (size_t)kRingBytes + (size_t)(2 * kMaxSlots) * 8 + (size_t)(2 * kMaxWarps) * sizeof(WPart);
 }
 static_assert(train_smem_bytes() <= 227 * 1024, "shared memory budget");
 
@@ -678,36 +729,121 @@ int k7_config(int64_t row_bytes) {
   return row_bytes <= 160 * 1024 ? kK7TwoGroups : kK7Default;
 }
 
+// ---- k_train_rows: the fp64 row end of K7 ---------------------------------------
+// One lane per row: merges the row's K warp partials in fp64 (warp order),
+// row_stats / row_loss (rowmath.cuh), writes logp / entropy, and adds the loss
+// partials with the fixed-order scheme of K4 (k_loss): per-lane fp64 sums over
+// a fixed tile assignment, per-turn buckets accumulated in lane order, warps
+// merged in order into one slab row per CTA. Deterministic run to run. Moving
+// this off K7 keeps its fp64 transcendentals (~1.2k cycles of latency per row)
+// and the partial bookkeeping away from the row group's critical path.
+constexpr int kRowsWarps = 8;
+
+template <int K>
+__global__ void __launch_bounds__(kRowsWarps * 32) k_train_rows(const TrainArgs p, double* slab, int accumulate) {
+  __shared__ double g_w[kRowsWarps * kNG];
+  __shared__ double bk_w[kRowsWarps * kBucketDoubles];
+  __shared__ int s_key[kRowsWarps][32];
+  __shared__ double s_val[kRowsWarps][32][PRORL_N_PER_TURN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = lane; t < kBucketDoubles; t += 32) bk_w[warp * kBucketDoubles + t] = 0.0;
+  double g[kNG];
+#pragma unroll
+  for (int k = 0; k < kNG; ++k) g[k] = 0.0;
+  const WPart* parts = static_cast<const WPart*>(p.parts);
+  const int64_t gw = (int64_t)blockIdx.x * kRowsWarps + warp, nw = (int64_t)gridDim.x * kRowsWarps;
+  const int64_t n_tiles = (p.n_rows + 31) / 32;
+  __syncwarp();
+  for (int64_t tile = gw; tile < n_tiles; tile += nw) {
+    const int64_t i = tile * 32 + lane;
+    int key = -1;
+    if (i < p.n_rows) {
+      const WPart m = merge_parts_f64<K>(parts + i * K, p.c);
+      const RowStats rs = row_stats(m.Mc, m.Mx, m.S, m.T, p.xy[i], p.c, (double)p.inv_temp);
+      if (p.logp) p.logp[i] = (float)rs.logp;
+      if (p.entropy) p.entropy[i] = (float)rs.ent;
+      const float old = p.old_lp[i];
+      int k = p.row_turn[i];
+      key = k < 0 ? 0 : (k >= p.n_buckets ? p.n_buckets - 1 : k);
+      const RowLoss rl = row_loss(rs.logp, old, p.adv[p.row_seq[i]], p.lo_d, p.hi_d, p.ref_lp, i, (double)p.kl_coef);
+      g[0] += rl.loss;
+      g[1] += 1.0;
+      g[2] += rs.ent;
+      g[3] += rs.logp;
+      g[4] += rl.ratio;
+      g[5] += rl.clip_lo;
+      g[6] += rl.clip_hi;
+      g[7] += (double)old - rs.logp;
+      g[10] += rl.kl;
+      s_val[warp][lane][0] = 1.0;
+      s_val[warp][lane][1] = rl.loss;
+      s_val[warp][lane][2] = rs.ent;
+      s_val[warp][lane][3] = rs.logp;
+      s_val[warp][lane][4] = rl.clip_lo + rl.clip_hi;
+    }
+    s_key[warp][lane] = key;
+    __syncwarp();
+    if (lane < PRORL_N_PER_TURN) {  // fixed-order per-turn accumulation
+      for (int src = 0; src < 32; ++src) {
+        const int kk = s_key[warp][src];
+        if (kk >= 0) bk_w[warp * kBucketDoubles + kk * PRORL_N_PER_TURN + lane] += s_val[warp][src][lane];
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < kNG; ++k) {
+    const double v = warp_sum_d(g[k]);
+    if (lane == 0) g_w[warp * kNG + k] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < PRORL_N_PARTIALS; t += blockDim.x) {
+    double v = 0.0;
+    if (t < kNG) {
+      for (int w = 0; w < kRowsWarps; ++w) v += g_w[w * kNG + t];
+    } else if (t >= PRORL_N_GLOBAL) {
+      for (int w = 0; w < kRowsWarps; ++w) v += bk_w[w * kBucketDoubles + (t - PRORL_N_GLOBAL)];
+    }
+    double* dst = slab + (size_t)blockIdx.x * PRORL_N_PARTIALS + t;
+    *dst = accumulate ? *dst + v : v;
+  }
+}
+
 template <typename T, int W, int UNIT, int G = 1, bool SELF = false>
-int run_train_cfg(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
+int run_train_cfg(const TrainArgs& a, int n_sm, double* slab, int accumulate, int* rows_used, cudaStream_t st) {
   constexpr int SUBV_BF16 = UNIT / 512 >= 8 ? 8 : UNIT / 512;
   auto kern = k_train<T, sizeof(T) == 2 ? SUBV_BF16 : 4, W, UNIT, G, SELF>;
   constexpr size_t smem = train_smem_bytes();
   PRORL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)std::min<int64_t>((int64_t)n_sm, a.n_rows);
-  *rows_used = grid;
-  kern<<<grid, (W + (SELF ? 0 : G)) * 32, smem, st>>>(a);
+  kern<<<grid, (W + (SELF ? 0 : 1)) * 32, smem, st>>>(a);
   PRORL_CUDA(cudaGetLastError());
+  // the row end: fp64 stats, outputs and the loss partials (slab rows [0, rgrid))
+  const int64_t tiles = (a.n_rows + 31) / 32;
+  const int rgrid = (int)std::min<int64_t>((int64_t)n_sm, (tiles + kRowsWarps - 1) / kRowsWarps);
+  k_train_rows<W / G><<<rgrid, kRowsWarps * 32, 0, st>>>(a, slab, accumulate);
+  PRORL_CUDA(cudaGetLastError());
+  *rows_used = rgrid;
   return PRORL_OK;
 }
 
 template <typename T>
-int run_train(const TrainArgs& a, int n_sm, int* rows_used, cudaStream_t st) {
+int run_train(const TrainArgs& a, int n_sm, double* slab, int accumulate, int* rows_used, cudaStream_t st) {
   switch (k7_config((int64_t)a.vocab * (int64_t)sizeof(T))) {
-    case kK7TwoGroups: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, rows_used, st);
-    case kK7FourGroups: return run_train_cfg<T, 16, 4096, 4>(a, n_sm, rows_used, st);
+    case kK7TwoGroups: return run_train_cfg<T, 16, 4096, 2>(a, n_sm, slab, accumulate, rows_used, st);
+    case kK7FourGroups: return run_train_cfg<T, 16, 4096, 4>(a, n_sm, slab, accumulate, rows_used, st);
 #ifdef PRORL_TUNING
-    case 0: return run_train_cfg<T, 16, 4096>(a, n_sm, rows_used, st);
-    case 2: return run_train_cfg<T, 24, 2048>(a, n_sm, rows_used, st);
-    case 3: return run_train_cfg<T, 12, 4096>(a, n_sm, rows_used, st);
-    case 4: return run_train_cfg<T, 24, 4096>(a, n_sm, rows_used, st);
-    case 6: return run_train_cfg<T, 16, 2048, 2>(a, n_sm, rows_used, st);
-    case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, rows_used, st);
-    case 8: return run_train_cfg<T, 16, 4096, 1, true>(a, n_sm, rows_used, st);
-    case 9: return run_train_cfg<T, 16, 4096, 2, true>(a, n_sm, rows_used, st);
-    case 11: return run_train_cfg<T, 16, 4096, 4, true>(a, n_sm, rows_used, st);
+    case 0: return run_train_cfg<T, 16, 4096>(a, n_sm, slab, accumulate, rows_used, st);
+    case 2: return run_train_cfg<T, 24, 2048>(a, n_sm, slab, accumulate, rows_used, st);
+    case 3: return run_train_cfg<T, 12, 4096>(a, n_sm, slab, accumulate, rows_used, st);
+    case 4: return run_train_cfg<T, 24, 4096>(a, n_sm, slab, accumulate, rows_used, st);
+    case 6: return run_train_cfg<T, 16, 2048, 2>(a, n_sm, slab, accumulate, rows_used, st);
+    case 7: return run_train_cfg<T, 8, 4096>(a, n_sm, slab, accumulate, rows_used, st);
+    case 8: return run_train_cfg<T, 16, 4096, 1, true>(a, n_sm, slab, accumulate, rows_used, st);
+    case 9: return run_train_cfg<T, 16, 4096, 2, true>(a, n_sm, slab, accumulate, rows_used, st);
+    case 11: return run_train_cfg<T, 16, 4096, 4, true>(a, n_sm, slab, accumulate, rows_used, st);
 #endif
-    default: return run_train_cfg<T, 16, 2048>(a, n_sm, rows_used, st);  // kK7Default
+    default: return run_train_cfg<T, 16, 2048>(a, n_sm, slab, accumulate, rows_used, st);  // kK7Default
   }
 }
 
@@ -760,10 +896,13 @@ int launch_train(prorl_ctx* ctx, const void* logits, int dtype, int64_t row_stri
   a.logp = logp;
   a.entropy = entropy;
   a.dlogp = dlogp;
-  a.slab = slab;
-  a.accumulate = accumulate ? 1 : 0;
-  return dtype == PRORL_BF16 ? run_train<__nv_bfloat16>(a, ctx->n_sm, rows_used, st)
-                             : run_train<float>(a, ctx->n_sm, rows_used, st);
+  // row-end workspace: each row's fp64 warp partials (<= kMaxWarps) + its target logit
+  PRORL_CUDA(ctx->k7rows.ensure((size_t)n_rows * (kMaxWarps * sizeof(WPart) + sizeof(float))));
+  a.parts = ctx->k7rows.p;
+  a.xy = reinterpret_cast<float*>(static_cast<uint8_t*>(ctx->k7rows.p) + (size_t)n_rows * kMaxWarps * sizeof(WPart));
+  const int acc = accumulate ? 1 : 0;
+  return dtype == PRORL_BF16 ? run_train<__nv_bfloat16>(a, ctx->n_sm, slab, acc, rows_used, st)
+                             : run_train<float>(a, ctx->n_sm, slab, acc, rows_used, st);
 }
 
 }  // namespace prorl
