@@ -36,6 +36,15 @@ def test_reference_arm_json():
     assert d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
     _check_e2e(d)
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the same config dict our arm prints for this workload (it names the workload; "run" says how)
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2603_18815_b200 import synth
+    c = synth.CONFIGS["c1"]
+    g = bench.global_workload(c, 1, "weak")
+    sh = synth.make_shard(g, seed=2603 + c["index"])
+    assert d["config"] == bench.workload_config(c, "c1", g, 1, "weak", len(sh.groups), sh.n_active)
+    assert d["cpu_baseline"]["timing"] == "wall clock" and d["cpu_baseline"]["cpu_model"]
 
 
 @pytest.mark.gpu
