@@ -72,17 +72,28 @@ def bytes_per_row(vocab: int, dtype: str) -> int:
     return vocab * (2 if dtype == "bf16" else 4) + 26
 
 
-K_SCORE_SOURCES = ("score.cu", "rowmath.cuh", "stream.cuh", "common.cuh")
+K_SCORE_FN = "k_scoreI13__nv_bfloat16Li16ELi2ELi4096ELi8ELb1E"  # the default fused bf16 K2+K4 instantiation
 
 
-def k_score_stamp() -> str:
-    """Digest of the sources k_score is compiled from: an ncu traffic capture is
-    only quoted for the kernel build it was taken on."""
+def k_score_stamp() -> str | None:
+    """Digest of the SASS of the k_score instantiation the bench runs, read
+    from the built library (cuobjdump): an ncu traffic capture is quoted only
+    for the kernel binary it was taken on."""
     import hashlib
-    h = hashlib.sha256()
-    for f in K_SCORE_SOURCES:
-        h.update((ROOT / "paper_2603_18815_b200" / "csrc" / f).read_bytes())
-    return h.hexdigest()[:16]
+    lib = ROOT / "paper_2603_18815_b200" / "libprorl_hotpath.so"
+    tool = "/usr/local/cuda/bin/cuobjdump" if Path("/usr/local/cuda/bin/cuobjdump").exists() else "cuobjdump"
+    try:
+        out = subprocess.run([tool, "-sass", str(lib)], capture_output=True, text=True, timeout=60).stdout
+    except Exception:
+        return None
+    h, on, n = hashlib.sha256(), False, 0
+    for line in out.splitlines():
+        if "Function :" in line:
+            on = K_SCORE_FN in line
+        elif on and line.strip():
+            h.update(line.strip().encode())
+            n += 1
+    return h.hexdigest()[:16] if n else None
 
 
 def k_score_traffic(rows_per_launch: int):
@@ -96,9 +107,10 @@ def k_score_traffic(rows_per_launch: int):
         tj = json.loads(tf.read_text())
     except Exception as ex:
         return None, f"unreadable capture: {ex!r}"
-    if tj.get("source_stamp") != k_score_stamp():
-        return None, "stale capture: k_score sources changed since profiles/k_score_traffic.json"
-    return tj["dram_bytes_per_row"] * rows_per_launch, f"ncu capture {tj.get('source', '?')} (source stamp matches)"
+    stamp = k_score_stamp()
+    if stamp is None or tj.get("sass_stamp") != stamp:
+        return None, "stale capture: the k_score binary differs from the one profiles/k_score_traffic.json was taken on"
+    return tj["dram_bytes_per_row"] * rows_per_launch, f"ncu capture {tj.get('source', '?')} (kernel SASS stamp matches)"
 
 
 def measured_peak_gbs():

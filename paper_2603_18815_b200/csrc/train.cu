@@ -489,8 +489,13 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : 1)) * 32, 1) k_train(const Tr
 
     // ---- pass A: statistics ----
     Top top{-INFINITY, 0.f};
-    LaneSums acc;  // ~5 units per warp and row: <= ~40 terms per fp32 sum, folded to fp64 at the row end
+    // fp32 sums over <= 128 elements per lane (32 per accumulator), folded into
+    // fp64: a 256 K-vocabulary row (16 units per warp) summed 128 terms per
+    // accumulator in fp32 and carried a -8e-9 logp bias
+    constexpr int kFoldUnits = (128 / (kUnit / ES / 32)) > 0 ? 128 / (kUnit / ES / 32) : 1;
+    LaneSums acc;
     acc.zero();
+    int nu = 0;  // units this warp has summed in this row
     for (int k = first_piece(pcb); k < g.npc; k += kPG) {
       const uint32_t pc = pcb + (uint32_t)k;
       const int u = k * kSplit + kk;
@@ -522,11 +527,12 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : 1)) * 32, 1) k_train(const Tr
         // fp32 exact enough, and most of a warp's ~5 units per row skip the
         // raise + exclusion path (see the note at kRaiseSlack)
         if (__any_sync(kFull, lm * c > top.Mc + kRaiseSlack)) {
-          const int L = raise_top<false>(lm, c, top, acc, lane);  // no fp64 fold before the row end
+          const int L = raise_top(lm, c, top, acc, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(w, top.Mx);
         }
         Elem<T>::template accumulate<SUBV>(w, c2, make_float2(-top.Mc, -top.Mc), acc.S, acc.T);
       }
+      if (++nu % kFoldUnits == 0) acc.fold();
     }
     if (wq == 0 && g.head + g.tail > 0) {
       const int64_t idx = edge_index<ES>(g, lane);

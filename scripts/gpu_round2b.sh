@@ -12,6 +12,7 @@ timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/b
 tail -c 1500 gpurun_out/bench_ref.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_score -s 3 -c 1 -o gpurun_out/prof_k_score_r02 \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-backward > gpurun_out/prof_k_score_r02.log 2>&1; echo ncu rc=$?
+python -c "import bench; print(bench.k_score_stamp())" > gpurun_out/k_score_sass_stamp.txt  # the binary the capture is of
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-backward > gpurun_out/launches_r02.log 2>&1; echo launches rc=$?
 ls -la gpurun_out

@@ -72,10 +72,18 @@ def full(rep: str, rows_per_launch: int, traffic_out: str | None) -> None:
         # stamped with the digest of the kernel's sources: bench.py quotes the
         # capture only while the sources are the ones it was taken on
         sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
-        from bench import k_score_stamp
+        # the SASS digest of the binary the capture was taken on (written next to
+        # the report on the GPU box by scripts/gpu_round2b.sh), else of the local build
+        import pathlib
+        stamp_file = pathlib.Path(rep).with_name("k_score_sass_stamp.txt")
+        if stamp_file.exists():
+            stamp = stamp_file.read_text().strip()
+        else:
+            from bench import k_score_stamp
+            stamp = k_score_stamp()
         json.dump({"source": rep.split("/")[-1], "kernel": names[0], "rows_per_launch": rows_per_launch,
                    "dram_bytes_per_launch": rd + wr, "dram_bytes_per_row": per_row,
-                   "source_stamp": k_score_stamp()}, open(traffic_out, "w"), indent=1)
+                   "sass_stamp": stamp}, open(traffic_out, "w"), indent=1)
 
 
 def launches(path: str) -> None:
