@@ -12,27 +12,34 @@
 //     ONE row at a time, so the rows in flight (148 x G x 2V bytes: 45 MB at
 //     V = 151 936 bf16) fit in the 126 MB L2 between the two passes over each
 //     row, and one group's barrier and pipeline bubbles overlap the others'.
-//   * Pass A (statistics): the group's producer warp streams the row from HBM
-//     into the group's shared-memory ring of 16 KB pieces (1-D TMA bulk
-//     copies; L2 evict_last on the pieces pass B re-reads). Piece P goes to a
-//     fixed set of kSplit warps, one 2 or 4 KB unit each (config), so every
-//     warp sees every round of its ring slots in
+//   * Pass A (statistics): one producer warp (lane g feeds group g) streams
+//     each group's row from HBM into the group's shared-memory ring of 16 KB
+//     pieces (1-D TMA bulk copies; L2 evict_last on the pieces pass B
+//     re-reads). Piece P goes to a fixed set of kSplit warps, one 2 or 4 KB
+//     unit each (config), so every warp sees every round of its ring slots in
 //     order (a parity wait never aliases a round two phases back; pieces can
-//     complete out of order). Warps run K2's online base-2 logsumexp
-//     (warp-uniform running max, top element kept out of the sums); the warp
-//     partials meet in shared memory after one named barrier and every warp
-//     merges them with the same fixed tree, so all hold bit-identical lse /
-//     logp / loss terms.
+//     complete out of order). Warps run K2's online base-2 logsumexp with
+//     the row arithmetic of rowmath.cuh (integer running reference, fp32
+//     lane sums folded into fp64 every 128 elements per lane, fp64 warp
+//     sums); the warp partials meet in shared memory after one named barrier.
+//     Each warp merges them with the same fixed fp32 tree (bit-identical lse
+//     for the gradient); warp 0 stores the fp64 warp partials and the target
+//     logit of the row for the row end.
 //   * Pass B (gradient): the last ring-full of pass-A pieces is still in
 //     shared memory and is consumed first, straight from there (pass A holds
 //     those slots); the rest of the row is streamed again — from L2
 //     (evict_first) — into the slots they free. Warps write
 //     grad = s (1[v = y] - p_v) as 16-B streaming stores. The producer runs
 //     ahead across passes and rows. (Rows of <= 192 KB never leave shared
-//     memory between the passes.)
-//   * One lane per group keeps the loss epilogue (fp64 partials + per-turn
-//     buckets, fixed order); the groups' sums merge in fixed order into one
-//     slab row per CTA (deterministic).
+//     memory between the passes.) The clip decision of s is taken in fp32
+//     except within a few ulp of the clip edge, where the fp64 merge decides
+//     (unclipped_f64), so gradient and loss agree on every row.
+//   * Row end (k_train_rows, one lane per row, launched after K7): merges the
+//     row's fp64 warp partials exactly, derives lse / logp / entropy and the
+//     DAPO / KL terms in fp64 (row_stats / row_loss, as K2's epilogue) and
+//     accumulates them in fixed order into one slab row per CTA
+//     (deterministic). Keeping the fp64 work out of K7 keeps K7's registers
+//     and issue slots on the stream (an in-kernel fp64 epilogue cost 4-18 %).
 //
 // Any row layout K2/K5 accept works: the 16-B aligned interior of each row goes
 // through TMA, the < 16-B head/tail elements are handled by warp 0 directly;
@@ -591,8 +598,8 @@ __global__ void __launch_bounds__((W + (SELF ? 0 : 1)) * 32, 1) k_train(const Tr
     Gp.S = __shfl_sync(kFull, Gp.S, 0);
 
     // ---- row results ----
-    // fp32 for the gradient (every warp; one bf16 rounding of tolerance), fp64
-    // for the outputs and the loss partials (warp 0, lane 0, below)
+    // fp32 for the gradient (every warp; one bf16 rounding of tolerance); the
+    // fp64 outputs and loss partials come from k_train_rows
     const float rr = fmaf(Gp.Mx, c, -Gp.Mc);
     const float ir = ex2_approx(-rr);
     const float qq = Gp.S * ir;

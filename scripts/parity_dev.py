@@ -28,7 +28,7 @@ from paper_2603_18815_b200 import synth  # noqa: E402
 from paper_2603_18815_b200.hotpath import ScoreConfig, Scorer  # noqa: E402
 
 sys.path.insert(0, str(ROOT / "tests" / "golden"))
-from make_full_partials import CASES, SEED, SIGMA, batch_digest, case_config  # noqa: E402
+from make_full_partials import CASES, SEED, SIGMA, batch_digest, case_config, case_opts  # noqa: E402
 
 
 def rows_vs_oracle(s: Scorer, dev) -> dict:
@@ -76,7 +76,7 @@ def main() -> None:
         sh = synth.make_shard(c["config"], **c["kw"])
         b = sh.batch.pinned()
         cc = case_config(name)
-        cfg = ScoreConfig(vocab=cc["vocab"], dtype=cc["dtype"], microbatch_rows=16576)
+        cfg = ScoreConfig(vocab=cc["vocab"], dtype=cc["dtype"], microbatch_rows=16576, **case_opts(name))
         tdt = torch.bfloat16 if cc["dtype"] == "bf16" else torch.float32
         pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=tdt, device=dev) for _ in range(2)]
         fwd, tm = s.score_host(b, cfg, pool, fill=True, seed=SEED, sigma=SIGMA)
