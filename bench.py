@@ -593,6 +593,7 @@ def run_ours(args):
         seg += tm
     ev1.record(stream)
     torch.cuda.synchronize()
+    step_info = sc.last_step_info()  # the library's own count of what the last timed step launched / copied
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -649,7 +650,7 @@ def run_ours(args):
                                            "seconds")}
             except Exception as ex:  # the baseline must not sink the GPU number
                 cpu = {"error": repr(ex)}
-        launches_per_step = 6 + 3 + 1 + n_mb + 1 + 1  # 2 scans x3, seq_bounds/pack/compact, grpo, score x n_mb, reduce, fold-errors
+        launches_per_step = step_info["kernel_launches"]  # K1 (turn scan + per-chunk token pass), K3, K2+K4 x n_mb, reduce, fold
         line = {
             "metric": "masked tokens/sec scored (logprob+GRPO loss)",
             "value": value, "unit": "masked tokens/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -658,7 +659,7 @@ def run_ours(args):
             "config": workload_config(c, args.config, gcfg, world, args.scaling, n_groups, n_total),
             "run": {"lpt_imbalance_max_over_mean": lpt_imbalance, "rank0_groups": len(shard.groups),
                     "rank0_active_rows": shard.n_active, "microbatch_rows": args.microbatch,
-                    "micro_batches_per_step": n_mb, "logits_pool": f"{args.pool} x {args.microbatch} rows "
+                    "micro_batches_per_step": n_mb, "h2d_chunks": step_info["h2d_chunks"], "logits_pool": f"{args.pool} x {args.microbatch} rows "
                     f"({args.pool * args.microbatch * c['vocab'] * (2 if c['dtype'] == 'bf16' else 4) / 1e9:.1f} GB)",
                     "l2": "inputs larger than L2 (logits pool >> 126 MB; no flush needed)"},
             "e2e": {"value": e2e, "unit": "masked tokens/s", "h2d_bytes_per_step": host.bytes_h2d(),

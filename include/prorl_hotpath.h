@@ -358,8 +358,16 @@ typedef struct prorl_logits_pool {
 /* Full per-GPU step from HOST buffers: H2D of the SoA, K1 pack, K3 GRPO, for
  * each micro-batch K2+K4 (fused), NCCL all-reduce (if initialised), D2H of
  * the partials into host_partials[PRORL_N_PARTIALS]. Synchronises `stream`.
- * timings_ms (nullable, [5]): h2d, pack+grpo, score (K2+K4 launches + slab
- * reduce, incl. generation when pool->fill), allreduce, d2h.
+ * The token SoA (ids, lp) is copied in chunks of whole sequences on an
+ * internal copy stream, and each chunk is packed just before the first
+ * micro-batch that needs it, so the copy overlaps the scoring launches (not
+ * in training mode with consume_grad: every token is checked before the
+ * first gradient leaves). Host buffers must stay valid until the call returns
+ * (it does not return before the copies are done); pinned memory overlaps.
+ * timings_ms (nullable, [5]): h2d (the descriptors, rewards and — when not
+ * chunked — the token SoA), pack+grpo (incl. the wait for the first chunk),
+ * score (K2+K4 launches + slab reduce, incl. generation when pool->fill and
+ * the later chunks' packing), allreduce, d2h.
  * Collective-safe failure: with a communicator of > 1 ranks every rank takes
  * part in exactly one all-reduce per call, even when its own step fails
  * (host validation, a callback, a device-side check): it contributes zeros
@@ -377,6 +385,13 @@ int prorl_score_host(prorl_ctx* ctx, const prorl_host_batch* batch, const prorl_
  * this rank — its own error, PRORL_E_PEER_FAILED if any other rank failed, or
  * PRORL_OK. Host-only, no ctx. */
 void prorl_fail_partials(double* host_partials);
+/* What the last prorl_score_host call on ctx did (diagnostics): kernels this
+ * library launched (callbacks' and NCCL's work not counted), micro-batches,
+ * the chunks the token SoA was copied in, and the H2D bytes. */
+typedef struct prorl_step_info {
+  int64_t kernel_launches; int32_t micro_batches; int32_t h2d_chunks; int64_t h2d_bytes;
+} prorl_step_info;
+int prorl_last_step_info(const prorl_ctx* ctx, prorl_step_info* out);
 int prorl_step_status(int local_status, const double* reduced_host_partials);
 
 #ifdef __cplusplus

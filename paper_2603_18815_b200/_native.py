@@ -38,6 +38,7 @@ EXPORTS = [
     "prorl_score_rows", "prorl_nccl_unique_id", "prorl_nccl_init", "prorl_allreduce", "prorl_gen_logits",
     "prorl_gen_logits_keyed", "prorl_row_keys", "prorl_logits_grad", "prorl_score_grad", "prorl_lmhead_logprob", "prorl_ingest_responses", "prorl_ingest_free",
     "prorl_synth_rewards", "prorl_shard_lpt", "prorl_score_host", "prorl_fail_partials", "prorl_step_status",
+    "prorl_last_step_info",
 ]
 
 vp = C.c_void_p
@@ -62,6 +63,11 @@ class HostBatch(C.Structure):
     _fields_ = [("turns", vp), ("n_turns", C.c_int64), ("ids", vp), ("lp", vp), ("n_tokens", C.c_int64),
                 ("reward", vp), ("usable", vp), ("n_rollouts", C.c_int32), ("group_off", vp),
                 ("n_groups", C.c_int32), ("rollout_key", vp)]
+
+
+class StepInfo(C.Structure):
+    _fields_ = [("kernel_launches", C.c_int64), ("micro_batches", C.c_int32), ("h2d_chunks", C.c_int32),
+                ("h2d_bytes", C.c_int64)]
 
 
 class IngestResult(C.Structure):
@@ -124,6 +130,7 @@ def _load() -> C.CDLL:
         "prorl_shard_lpt": (C.c_int, [i32, vp, i32, vp]),
         "prorl_fail_partials": (None, [vp]),
         "prorl_step_status": (C.c_int, [C.c_int, vp]),
+        "prorl_last_step_info": (C.c_int, [vp, C.POINTER(StepInfo)]),
         "prorl_score_host": (C.c_int, [vp, C.POINTER(HostBatch), C.POINTER(ScoreCfg), C.POINTER(LogitsPool), vp, vp,
                                        vp]),
     }

@@ -118,6 +118,62 @@ static int64_t host_active_rows(const prorl_turn_desc* turns, int64_t n_turns) {
   return n;
 }
 
+// prorl_score_host's H2D chunks: packed tokens [p0, p1) (whole sequences),
+// their active rows [a0, a1), and the host SoA range [s0, s1) they read.
+struct PackChunk {
+  int64_t p0, p1, a0, a1, s0, s1;
+};
+
+// Split the turn list at sequence starts into at most max_chunks chunks of
+// doubling size, the first holding about one micro-batch of active rows (it is
+// the only copy the scoring waits for). Falls back to one chunk covering the
+// whole SoA when the chunks' source ranges overlap by more than 1/8 of it
+// (turns that do not read the SoA in order).
+static int plan_chunks(const prorl_turn_desc* turns, int64_t n_turns, int64_t n_tokens, int64_t n_active,
+                       int64_t mb_rows, int max_chunks, PackChunk* out) {
+  out[0] = PackChunk{0, n_tokens, 0, n_active, 0, n_tokens};
+  if (max_chunks < 2 || n_active <= mb_rows) return 1;
+  int64_t target = std::max<int64_t>(
+      {n_tokens / 64, 1, (int64_t)((double)mb_rows * (double)n_tokens / (double)n_active)});
+  int n = 0;
+  PackChunk cur{0, 0, 0, 0, INT64_MAX, 0};
+  int64_t p = 0, a = 0, pos = 0, copied = 0;
+  int32_t traj = -1;
+  for (int64_t t = 0; t < n_turns; ++t) {
+    const prorl_turn_desc& d = turns[t];
+    if (d.traj != traj) {  // a sequence starts at packed token p
+      if (p - cur.p0 >= target && n < max_chunks - 1) {
+        cur.p1 = p;
+        cur.a1 = a;
+        if (cur.s0 > cur.s1) cur.s0 = cur.s1 = 0;
+        copied += cur.s1 - cur.s0;
+        out[n++] = cur;
+        cur = PackChunk{p, p, a, a, INT64_MAX, 0};
+        target *= 2;
+      }
+      traj = d.traj;
+      pos = 0;
+    }
+    if (d.len > 0) {
+      cur.s0 = std::min(cur.s0, d.src_off);
+      cur.s1 = std::max(cur.s1, d.src_off + d.len);
+      if (d.role == PRORL_ROLE_ASSISTANT) a += d.len - (pos == 0 ? 1 : 0);
+    }
+    pos += d.len;
+    p += d.len;
+  }
+  cur.p1 = p;
+  cur.a1 = a;
+  if (cur.s0 > cur.s1) cur.s0 = cur.s1 = 0;
+  copied += cur.s1 - cur.s0;
+  out[n++] = cur;
+  if (n < 2 || copied > n_tokens + n_tokens / 8) {
+    out[0] = PackChunk{0, n_tokens, 0, n_active, 0, n_tokens};
+    return 1;
+  }
+  return n;
+}
+
 }  // namespace prorl
 
 using namespace prorl;
@@ -164,7 +220,15 @@ int prorl_ctx_create(int device, prorl_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(int) * ERR_N);
   if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int) * ERR_N);
   for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  for (int i = 0; i <= prorl_ctx::kMaxChunks && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&c->chunk_ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
+    for (auto& ev : c->ev)
+      if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->chunk_ev)
+      if (ev) cudaEventDestroy(ev);
+    if (c->d_err) cudaFree(c->d_err);
     delete c;
     return cuda_fail(e, "prorl_ctx_create");
   }
@@ -184,6 +248,9 @@ int prorl_ctx_destroy(prorl_ctx* c) {
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : c->chunk_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->d_err) cudaFree(c->d_err);
   delete c;
   return PRORL_OK;
@@ -424,6 +491,12 @@ int prorl_score_host(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score
   return fail(rc, msg);
 }
 
+int prorl_last_step_info(const prorl_ctx* c, prorl_step_info* out) {
+  if (!c || !out) return fail(PRORL_E_MALFORMED_REQUEST, "prorl_last_step_info: null argument");
+  *out = c->last_step;
+  return PRORL_OK;
+}
+
 void prorl_fail_partials(double* host_partials) {
   if (!host_partials) return;
   std::memset(host_partials, 0, sizeof(double) * PRORL_N_PARTIALS);
@@ -534,27 +607,61 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   double* partials = c->partials.as<double>();
   double* slab = c->slab.as<double>();
   NvtxRange step_range("prorl_score_host");
+  prorl_step_info info{};
+  c->last_step = info;
+  // Token SoA chunks (one chunk = copied and packed before any scoring). In
+  // training mode with a gradient sink every token is checked before the first
+  // gradient leaves, so there the SoA is not chunked.
+  PackChunk chunks[prorl_ctx::kMaxChunks];
+  const int n_chunks = plan_chunks(hb->turns, hb->n_turns, N, A, cfg->microbatch_rows,
+                                   (train_mode && pool->consume_grad) ? 1 : prorl_ctx::kMaxChunks, chunks);
+  // The copy stream must be idle whenever this call returns (the caller may
+  // free or reuse its host buffers): joined on every exit path.
+  struct CopyJoin {
+    cudaStream_t s = nullptr;
+    ~CopyJoin() {
+      if (s) cudaStreamSynchronize(s);
+    }
+  } copy_join;
   PRORL_CUDA(cudaEventRecord(c->ev[0], st));
   // ---- H2D ----
-  if (hb->n_turns)
-    PRORL_CUDA(cudaMemcpyAsync(c->h_turns.p, hb->turns, sizeof(prorl_turn_desc) * hb->n_turns, cudaMemcpyHostToDevice, st));
-  if (N) {
-    PRORL_CUDA(cudaMemcpyAsync(c->h_ids.p, hb->ids, sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
-    PRORL_CUDA(cudaMemcpyAsync(c->h_lp.p, hb->lp, sizeof(double) * N, cudaMemcpyHostToDevice, st));
-  }
+  int64_t h2d = 0;
+  auto h2d_copy = [&](void* dst, const void* src, size_t bytes, cudaStream_t s) -> cudaError_t {
+    h2d += (int64_t)bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  if (hb->n_turns) PRORL_CUDA(h2d_copy(c->h_turns.p, hb->turns, sizeof(prorl_turn_desc) * hb->n_turns, st));
   if (R) {
-    PRORL_CUDA(cudaMemcpyAsync(c->h_reward.p, hb->reward, sizeof(double) * R, cudaMemcpyHostToDevice, st));
-    PRORL_CUDA(cudaMemcpyAsync(c->h_usable.p, hb->usable, (size_t)R, cudaMemcpyHostToDevice, st));
-    if (hb->rollout_key)
-      PRORL_CUDA(cudaMemcpyAsync(c->h_rkey.p, hb->rollout_key, sizeof(int64_t) * R, cudaMemcpyHostToDevice, st));
+    PRORL_CUDA(h2d_copy(c->h_reward.p, hb->reward, sizeof(double) * R, st));
+    PRORL_CUDA(h2d_copy(c->h_usable.p, hb->usable, (size_t)R, st));
+    if (hb->rollout_key) PRORL_CUDA(h2d_copy(c->h_rkey.p, hb->rollout_key, sizeof(int64_t) * R, st));
   }
-  if (G) PRORL_CUDA(cudaMemcpyAsync(c->h_goff.p, hb->group_off, sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice, st));
+  if (G) PRORL_CUDA(h2d_copy(c->h_goff.p, hb->group_off, sizeof(int32_t) * (G + 1), st));
+  if (N && n_chunks == 1) {
+    PRORL_CUDA(h2d_copy(c->h_ids.p, hb->ids, sizeof(int64_t) * N, st));
+    PRORL_CUDA(h2d_copy(c->h_lp.p, hb->lp, sizeof(double) * N, st));
+  } else if (N) {
+    // the staging buffers are free once the caller's earlier work on `st` is done
+    PRORL_CUDA(cudaEventRecord(c->chunk_ev[0], st));
+    copy_join.s = c->copy_stream;
+    PRORL_CUDA(cudaStreamWaitEvent(c->copy_stream, c->chunk_ev[0], 0));
+    for (int k = 0; k < n_chunks; ++k) {
+      const PackChunk& ch = chunks[k];
+      if (ch.s1 > ch.s0) {
+        PRORL_CUDA(h2d_copy(c->h_ids.as<int64_t>() + ch.s0, hb->ids + ch.s0, sizeof(int64_t) * (ch.s1 - ch.s0),
+                            c->copy_stream));
+        PRORL_CUDA(h2d_copy(c->h_lp.as<double>() + ch.s0, hb->lp + ch.s0, sizeof(double) * (ch.s1 - ch.s0),
+                            c->copy_stream));
+      }
+      PRORL_CUDA(cudaEventRecord(c->chunk_ev[k + 1], c->copy_stream));
+    }
+  }
   PRORL_CUDA(cudaMemsetAsync(partials, 0, sizeof(double) * PRORL_N_PARTIALS, st));
   PRORL_CUDA(cudaMemsetAsync(slab, 0, sizeof(double) * PRORL_N_PARTIALS * srows, st));
   PRORL_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int) * ERR_N, st));  // no stale flags from an aborted call
   PRORL_CUDA(cudaEventRecord(c->ev[1], st));
 
-  // ---- K1 pack, K3 grpo ----
+  // ---- K3 grpo, K1 pack (turn scan, then the token pass chunk by chunk) ----
   prorl_packed pk{};
   pk.tokens = c->p_tokens.as<int32_t>();
   pk.loss_mask = c->p_mask.as<uint8_t>();
@@ -569,11 +676,30 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   pk.act_seq = c->a_seq.as<int32_t>();
   pk.act_turn = c->a_turn.as<int16_t>();
   pk.n_active = c->a_nact.as<int64_t>();
-  PRORL_TRY(launch_pack(c, c->h_turns.as<prorl_turn_desc>(), hb->n_turns, c->h_ids.as<int64_t>(),
-                        c->h_lp.as<double>(), N, R, cfg->vocab, &pk, st));
+  const auto scan_launches = [](int64_t n) -> int64_t { return n > 0 ? 3 : 0; };
   PRORL_TRY(launch_grpo(c, c->h_reward.as<double>(), c->h_usable.as<uint8_t>(), c->h_goff.as<int32_t>(), G, cfg->ddof,
                         cfg->adv_eps, cfg->gate_tolerance, c->adv.as<double>(), c->informative.as<uint8_t>(), partials,
                         st));
+  info.kernel_launches += G > 0 ? 1 : 0;
+  PRORL_TRY(launch_pack_turns(c, c->h_turns.as<prorl_turn_desc>(), hb->n_turns, N, R, cfg->vocab, &pk, st));
+  info.kernel_launches += scan_launches(hb->n_turns) + 1;
+  int packed = 0;             // chunks packed so far
+  bool packed_since = false;  // a chunk was packed since the last scoring launch (no PDL across it)
+  // pack every chunk whose active rows start below `rows` (all chunks: INT64_MAX)
+  auto pack_upto = [&](int64_t rows) -> int {
+    for (; packed < n_chunks && (packed == 0 || chunks[packed].a0 < rows); ++packed) {
+      packed_since = true;
+      const PackChunk& ch = chunks[packed];
+      if (n_chunks > 1) PRORL_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[packed + 1], 0));
+      PRORL_TRY(launch_pack_tokens(c, c->h_turns.as<prorl_turn_desc>(), hb->n_turns, c->h_ids.as<int64_t>(),
+                                   c->h_lp.as<double>(), N, R, cfg->vocab, &pk, ch.p0, ch.p1, ch.a0,
+                                   packed == n_chunks - 1, st));
+      const bool last = packed == n_chunks - 1;
+      if (ch.p1 > ch.p0 || last) info.kernel_launches += (ch.p1 > ch.p0 ? 1 : 0) + scan_launches(ch.p1 - ch.p0) + 1;
+    }
+    return PRORL_OK;
+  };
+  PRORL_TRY(pack_upto(0));
   PRORL_CUDA(cudaEventRecord(c->ev[2], st));
   // A gradient sink may apply what it is handed at once: make sure K1 accepted
   // every token id and descriptor before the first gradient leaves the library
@@ -585,6 +711,8 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   const double n_global = pool->n_global > 0.0 ? pool->n_global : (double)std::max<int64_t>(A, 1);
   for (int64_t j = 0, row0 = 0; row0 < A; ++j, row0 += mb) {
     const int64_t n = std::min(mb, A - row0);
+    PRORL_TRY(pack_upto(row0 + n));
+    ++info.micro_batches;
     const float* ref_lp = nullptr;  // k3 KL reference logprobs of this micro-batch
     if (pool->provide_ref && cfg->loss.kl_coef != 0.f) {
       const int rc = pool->provide_ref(pool->ref_user, row0, n, pk.act_row + row0, pk.act_seq + row0, pk.cu_seqlens,
@@ -611,6 +739,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
       PRORL_TRY(launch_loss(c, lp, en, pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0,
                             pk.act_turn + row0, ref_lp, n, &cfg->loss, slab, loss_slab_rows(c), &used, st));
       PRORL_TRY(launch_slab_reduce(slab, used, partials, st));
+      info.kernel_launches += 4;  // K6, its merge, K4, slab reduce
       continue;
     }
     const void* buf = nullptr;
@@ -630,6 +759,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
                                   hb->rollout_key ? c->h_rkey.as<int64_t>() : nullptr, n, keys, st));
         PRORL_TRY(prorl_gen_logits_keyed(c, b, cfg->dtype, pool->row_stride, cfg->vocab, n, keys,
                                          pk.act_target + row0, pk.act_old_lp + row0, pool->seed, pool->sigma, st));
+        info.kernel_launches += 2;
       }
       buf = b;
     }
@@ -644,6 +774,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
                              pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp,
                              n, cfg->inv_temperature, &cfg->loss, n_global, nullptr, nullptr, nullptr, grad, slab, true,
                              &used, st));
+      info.kernel_launches += 2;  // K7, its row end
       if (pool->consume_grad) {
         const int rc = pool->consume_grad(pool->grad_user, row0, n, grad, stride, stream);
         if (rc != PRORL_OK)
@@ -654,14 +785,22 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
     }
     // back-to-back scoring launches (resident pool: no callback or generator
     // work between them) overlap through programmatic dependent launch
-    const bool pdl = j > 0 && pdl_enabled() && !pool->provide && !pool->fill && !ref_lp;
+    // (not right after a K1 chunk: PDL would let the launch read the chunk's
+    // rows before K1 finished writing them)
+    const bool pdl = j > 0 && pdl_enabled() && !pool->provide && !pool->fill && !ref_lp && !packed_since;
+    packed_since = false;
     PRORL_TRY(launch_score(c, buf, cfg->dtype, stride, cfg->vocab, nullptr, pk.act_target + row0,
                            pk.act_old_lp + row0, c->adv.as<double>(), pk.act_seq + row0, pk.act_turn + row0, ref_lp, n,
                            cfg->inv_temperature, &cfg->loss, nullptr, nullptr, slab, srows, true, nullptr, st, pdl));
+    ++info.kernel_launches;
   }
+  PRORL_TRY(pack_upto(INT64_MAX));  // chunks without active rows (their packed tokens are still outputs)
   if (!lmhead_mode) PRORL_TRY(launch_slab_reduce(slab, srows, partials, st));
   k_fold_errors<<<1, 1, 0, st>>>(c->d_err, partials);
   PRORL_CUDA(cudaGetLastError());
+  info.kernel_launches += (lmhead_mode ? 0 : 1) + 1;
+  info.h2d_chunks = n_chunks;
+  info.h2d_bytes = h2d;
   PRORL_CUDA(cudaEventRecord(c->ev[3], st));
   reduced = true;  // from here on every rank has entered (or failed inside) the collective
   PRORL_TRY(prorl_allreduce(c, partials, PRORL_N_PARTIALS, stream));
@@ -669,6 +808,7 @@ int score_host_impl(prorl_ctx* c, const prorl_host_batch* hb, const prorl_score_
   PRORL_CUDA(cudaMemcpyAsync(host_partials, partials, sizeof(double) * PRORL_N_PARTIALS, cudaMemcpyDeviceToHost, st));
   PRORL_CUDA(cudaEventRecord(c->ev[5], st));
   PRORL_TRY(prorl_check_errors(c, stream));
+  c->last_step = info;
   PRORL_TRY(prorl_step_status(PRORL_OK, host_partials));
   if (timings_ms) {
     for (int k = 0; k < 5; ++k) PRORL_CUDA(cudaEventElapsedTime(&timings_ms[k], c->ev[k], c->ev[k + 1]));

@@ -117,6 +117,11 @@ struct prorl_ctx {
   void* nccl_comm = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0;
   cudaEvent_t ev[8] = {};
+  // prorl_score_host's chunked H2D of the token SoA (overlaps the scoring launches)
+  static constexpr int kMaxChunks = 8;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[kMaxChunks + 1] = {};  // [0]: the call's start on the caller's stream
+  prorl_step_info last_step{};
 };
 
 namespace prorl {
@@ -125,6 +130,15 @@ namespace prorl {
 int launch_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids,
                 const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab,
                 const prorl_packed* out, cudaStream_t st);
+// K1 in two phases: the turn scan (cu_seqlens; needs only the descriptors),
+// then the token pass over packed tokens [p0, p1) — a whole number of
+// sequences whose active rows start at a0 — so chunks can be packed as their
+// host data arrives. launch_pack = turns + tokens(0, n_tokens, 0, last).
+int launch_pack_turns(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, int64_t n_tokens, int32_t n_seq,
+                      int32_t vocab, const prorl_packed* out, cudaStream_t st);
+int launch_pack_tokens(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids,
+                       const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab, const prorl_packed* out,
+                       int64_t p0, int64_t p1, int64_t a0, bool last, cudaStream_t st);
 int launch_grpo(prorl_ctx* ctx, const double* reward, const uint8_t* usable, const int32_t* group_off,
                 int32_t n_groups, int32_t ddof, float eps, double tol, double* adv, uint8_t* informative,
                 double* partials, cudaStream_t st);

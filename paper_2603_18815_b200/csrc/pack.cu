@@ -63,16 +63,16 @@ __global__ void k_seq_bounds(const prorl_turn_desc* turns, int64_t n_turns, cons
   }
 }
 
-// One thread per token p: locate its turn (binary search over turn offsets),
-// convert id / logprob, emit mask, ids, and the active flag of row p-1.
+// One thread per token p in [p0, p1): locate its turn (binary search over turn
+// offsets), convert id / logprob, emit mask, ids, and the active flag of row
+// p-1 (flags[p1-1] stays 0 from the memset: p1 is a sequence start or the end).
 __global__ void k_pack_tokens(const prorl_turn_desc* __restrict__ turns, int64_t n_turns,
                               const int64_t* __restrict__ off, const int64_t* __restrict__ asst0,
-                              const int64_t* __restrict__ ids, const double* __restrict__ lp,
-                              int64_t n_tokens, int32_t n_seq, int32_t vocab, prorl_packed out, uint8_t* flags,
+                              const int64_t* __restrict__ ids, const double* __restrict__ lp, int64_t p0,
+                              int64_t p1, int32_t n_seq, int32_t vocab, prorl_packed out, uint8_t* flags,
                               int* err) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_tokens) return;
-  if (p == 0) flags[n_tokens - 1] = 0;
+  int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= p1) return;
   // largest t in [0, n_turns) with off_len[t] <= p
   int64_t lo = 0, hi = n_turns - 1;
   while (lo < hi) {
@@ -107,15 +107,17 @@ __global__ void k_pack_tokens(const prorl_turn_desc* __restrict__ turns, int64_t
   out.seq_id[p] = s;
   out.pos_id[p] = pos;
   out.old_lp[p] = asst ? __double2float_rn(lp[src]) : 0.0f;
-  if (p > 0) flags[p - 1] = (asst && pos > 0) ? 1 : 0;
+  if (p > p0) flags[p - 1] = (asst && pos > 0) ? 1 : 0;
 }
 
-__global__ void k_compact(const uint8_t* __restrict__ flags, const int32_t* __restrict__ pos,
-                          int64_t n_tokens, prorl_packed out) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) *out.n_active = (int64_t)pos[n_tokens];
-  if (r >= n_tokens || !flags[r]) return;
-  const int32_t i = pos[r];
+// Rows [p0, p1) with their chunk-local exclusive scan pos[0 .. p1-p0]; the
+// chunk's active rows start at a0. The last chunk writes the total.
+__global__ void k_compact(const uint8_t* __restrict__ flags, const int32_t* __restrict__ pos, int64_t p0,
+                          int64_t p1, int64_t a0, bool last, prorl_packed out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, r = p0 + k;
+  if (k == 0 && last) *out.n_active = a0 + (int64_t)pos[p1 - p0];
+  if (r >= p1 || !flags[r]) return;
+  const int32_t i = (int32_t)(a0 + pos[k]);
   out.act_row[i] = (int32_t)r;
   out.act_target[i] = out.tokens[r + 1];
   out.act_old_lp[i] = out.old_lp[r + 1];
@@ -127,45 +129,70 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 }  // namespace
 
-int launch_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids,
-                const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab, const prorl_packed* out,
-                cudaStream_t st) {
+namespace {
+// K1 workspace: off[n_turns+1] i64 | asst0[n_seq+1] i64 | act_pos[N+1] i32 | flags[N] u8
+struct PackWs {
+  int64_t* off;
+  int64_t* asst0;
+  int32_t* pos;
+  uint8_t* flags;
+  size_t total;
+  PackWs(uint8_t* base, int64_t n_turns, int32_t n_seq, int64_t n_tokens) {
+    const size_t o_asst = sizeof(int64_t) * (size_t)(n_turns + 1);
+    const size_t o_pos = o_asst + sizeof(int64_t) * (size_t)(n_seq + 1);
+    const size_t o_flag = o_pos + sizeof(int32_t) * (size_t)(n_tokens + 1);
+    total = o_flag + (size_t)n_tokens + 16;
+    off = reinterpret_cast<int64_t*>(base);
+    asst0 = reinterpret_cast<int64_t*>(base + o_asst);
+    pos = reinterpret_cast<int32_t*>(base + o_pos);
+    flags = base + o_flag;
+  }
+};
+}  // namespace
+
+int launch_pack_turns(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, int64_t n_tokens, int32_t n_seq,
+                      int32_t vocab, const prorl_packed* out, cudaStream_t st) {
   if (n_turns < 0 || n_tokens < 0 || n_seq < 0 || vocab <= 0)
     return fail(PRORL_E_SHAPE, "prorl_pack: negative size or vocab <= 0");
   if (n_tokens >= (int64_t(1) << 31) - 1)
     return fail(PRORL_E_SHAPE, "prorl_pack: more than 2^31-2 tokens per shard");
   if (n_tokens > 0 && n_turns == 0) return fail(PRORL_E_SHAPE, "prorl_pack: tokens without turns");
-  // workspace: off[n_turns+1] i64 | asst0[n_seq] i64 | act_pos[N+1] i32 | flags[N] u8
-  size_t o_off = 0;
-  size_t o_asst = o_off + sizeof(int64_t) * (size_t)(n_turns + 1);
-  size_t o_pos = o_asst + sizeof(int64_t) * (size_t)(n_seq + 1);
-  size_t o_flag = o_pos + sizeof(int32_t) * (size_t)(n_tokens + 1);
-  size_t total = o_flag + (size_t)n_tokens + 16;
-  PRORL_CUDA(ctx->pack_tmp.ensure(total));
-  size_t scan_elems = scan_tmp_elems(n_turns > n_tokens ? n_turns : n_tokens) + 1;
+  PRORL_CUDA(ctx->pack_tmp.ensure(PackWs(nullptr, n_turns, n_seq, n_tokens).total));
+  const size_t scan_elems = scan_tmp_elems(n_turns > n_tokens ? n_turns : n_tokens) + 1;
   PRORL_CUDA(ctx->scan_tmp.ensure(scan_elems * sizeof(int64_t)));
-  uint8_t* base = ctx->pack_tmp.as<uint8_t>();
-  int64_t* off = reinterpret_cast<int64_t*>(base + o_off);
-  int64_t* asst0 = reinterpret_cast<int64_t*>(base + o_asst);
-  int32_t* pos = reinterpret_cast<int32_t*>(base + o_pos);
-  uint8_t* flags = base + o_flag;
-
-  PRORL_CUDA(exclusive_scan<int64_t>(TurnVal{turns}, n_turns, off, ctx->scan_tmp.as<int64_t>(), st));
-  k_seq_bounds<<<blocks_for(n_turns + 1, 256), 256, 0, st>>>(turns, n_turns, off, n_seq, n_tokens,
-                                                               out->cu_seqlens, asst0, ctx->d_err);
-  PRORL_CUDA(cudaGetLastError());
-  if (n_tokens == 0) {
-    PRORL_CUDA(cudaMemsetAsync(out->n_active, 0, sizeof(int64_t), st));
-    return PRORL_OK;
-  }
-  PRORL_CUDA(cudaMemsetAsync(flags, 0, (size_t)n_tokens, st));
-  k_pack_tokens<<<blocks_for(n_tokens, 256), 256, 0, st>>>(turns, n_turns, off, asst0, ids, lp, n_tokens,
-                                                            n_seq, vocab, *out, flags, ctx->d_err);
-  PRORL_CUDA(cudaGetLastError());
-  PRORL_CUDA(exclusive_scan<int32_t>(FlagVal{flags}, n_tokens, pos, ctx->scan_tmp.as<int32_t>(), st));
-  k_compact<<<blocks_for(n_tokens, 256), 256, 0, st>>>(flags, pos, n_tokens, *out);
+  const PackWs w(ctx->pack_tmp.as<uint8_t>(), n_turns, n_seq, n_tokens);
+  PRORL_CUDA(exclusive_scan<int64_t>(TurnVal{turns}, n_turns, w.off, ctx->scan_tmp.as<int64_t>(), st));
+  k_seq_bounds<<<blocks_for(n_turns + 1, 256), 256, 0, st>>>(turns, n_turns, w.off, n_seq, n_tokens,
+                                                               out->cu_seqlens, w.asst0, ctx->d_err);
   PRORL_CUDA(cudaGetLastError());
   return PRORL_OK;
+}
+
+int launch_pack_tokens(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids,
+                       const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab, const prorl_packed* out,
+                       int64_t p0, int64_t p1, int64_t a0, bool last, cudaStream_t st) {
+  if (p0 < 0 || p1 < p0 || p1 > n_tokens) return fail(PRORL_E_SHAPE, "prorl_pack: token range outside [0, n_tokens]");
+  if (p1 == p0 && !last) return PRORL_OK;
+  const PackWs w(ctx->pack_tmp.as<uint8_t>(), n_turns, n_seq, n_tokens);
+  const int64_t n = p1 - p0;
+  if (n > 0) {
+    PRORL_CUDA(cudaMemsetAsync(w.flags + p0, 0, (size_t)n, st));
+    k_pack_tokens<<<blocks_for(n, 256), 256, 0, st>>>(turns, n_turns, w.off, w.asst0, ids, lp, p0, p1, n_seq, vocab,
+                                                       *out, w.flags, ctx->d_err);
+    PRORL_CUDA(cudaGetLastError());
+  }
+  PRORL_CUDA(exclusive_scan<int32_t>(FlagVal{w.flags + p0}, n, w.pos + p0, ctx->scan_tmp.as<int32_t>(), st));
+  // (the last chunk also writes n_active, even when it holds no tokens)
+  k_compact<<<n > 0 ? blocks_for(n, 256) : 1, 256, 0, st>>>(w.flags, w.pos + p0, p0, p1, a0, last, *out);
+  PRORL_CUDA(cudaGetLastError());
+  return PRORL_OK;
+}
+
+int launch_pack(prorl_ctx* ctx, const prorl_turn_desc* turns, int64_t n_turns, const int64_t* ids,
+                const double* lp, int64_t n_tokens, int32_t n_seq, int32_t vocab, const prorl_packed* out,
+                cudaStream_t st) {
+  PRORL_TRY_INTERNAL(launch_pack_turns(ctx, turns, n_turns, n_tokens, n_seq, vocab, out, st));
+  return launch_pack_tokens(ctx, turns, n_turns, ids, lp, n_tokens, n_seq, vocab, out, 0, n_tokens, 0, true, st);
 }
 
 }  // namespace prorl

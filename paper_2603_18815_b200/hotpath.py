@@ -269,6 +269,12 @@ class Scorer:
                                      _stream(stream)))
         return out, tm
 
+    def last_step_info(self) -> dict:
+        """What the last score_host call did: kernel launches, micro-batches, H2D chunks and bytes."""
+        si = N.StepInfo()
+        check(N.lib.prorl_last_step_info(self.ctx, C.byref(si)))
+        return {k: getattr(si, k) for k, _ in N.StepInfo._fields_}
+
     # ---- whole per-GPU step from host buffers ----
     def score_host(self, batch: "HostBatchArrays", cfg: ScoreConfig, pool: list[torch.Tensor], fill: bool,
                    seed: int = 0, sigma: float = 2.0, stream=None, train: bool = False, n_global: float = 0.0,

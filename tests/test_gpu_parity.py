@@ -337,6 +337,43 @@ def test_score_host_vs_oracle(scorer, cuda, config, kw):
     assert_partials_close(got, ref["partials"], ref["abs"], ref["n_border"], config)
     again, _ = scorer.score_host(b, cfg, pool, fill=True, seed=1234)
     assert np.array_equal(got, again)  # deterministic run to run
+    info = scorer.last_step_info()
+    assert info["micro_batches"] == -(-sh.n_active // cfg.microbatch_rows)
+    assert info["h2d_bytes"] >= 16 * b.ids.size and info["kernel_launches"] > info["micro_batches"]
+
+
+def _relaid(b: HostBatchArrays, order) -> HostBatchArrays:
+    """The same batch with the turns' tokens stored in the host SoA in another order."""
+    t = b.turns.copy()
+    ids, lp, off = [], [], 0
+    for k in order:
+        s0, L = int(b.turns["src_off"][k]), int(b.turns["len"][k])
+        ids.append(b.ids[s0:s0 + L])
+        lp.append(b.lp[s0:s0 + L])
+        t["src_off"][k] = off
+        off += L
+    return HostBatchArrays(t, np.concatenate(ids), np.concatenate(lp), b.reward, b.usable, b.group_off,
+                           rollout_key=b.rollout_key)
+
+
+def test_score_host_chunked_h2d_matches_single_copy(scorer, cuda):
+    """The token SoA is copied in chunks of whole sequences that overlap the
+    scoring (capi.cu plan_chunks). Storing the same turns in reverse order keeps
+    the chunks (disjoint source ranges); a random order falls back to one copy.
+    The packed batch is the same, so all three steps are bit-identical."""
+    sh = synth.make_shard("c1", seed=99)
+    b = sh.batch
+    cfg = _cfg("c1")
+    pool = [torch.empty((cfg.microbatch_rows, cfg.vocab), dtype=torch.float32, device=cuda) for _ in range(2)]
+    runs = {}
+    n_t = len(b.turns)
+    for name, order in (("stored", range(n_t)), ("reversed", range(n_t - 1, -1, -1)),
+                        ("shuffled", np.random.default_rng(5).permutation(n_t))):
+        bb = b if name == "stored" else _relaid(b, order)
+        runs[name] = scorer.score_host(bb.pinned(), cfg, pool, fill=True, seed=7)[0]
+        runs[name + "_chunks"] = scorer.last_step_info()["h2d_chunks"]
+    assert runs["stored_chunks"] > 1 and runs["reversed_chunks"] > 1 and runs["shuffled_chunks"] == 1
+    assert np.array_equal(runs["stored"], runs["reversed"]) and np.array_equal(runs["stored"], runs["shuffled"])
 
 
 def test_score_host_resident_pool_back_to_back(scorer, cuda):
