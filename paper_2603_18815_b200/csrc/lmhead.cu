@@ -53,12 +53,12 @@ struct LmParams {
   float c;           // inv_temp * log2 e
   const int32_t* targets;
   float* part;       // [n_rows][n_chunks][6]: Mc, Mx, S, T, xy, has_y
-  // Pacing (pair kernel, single wave over the whole vocabulary): producers
-  // publish each vocab tile they have issued in pace[tile] and do not issue
-  // tile n before every active worker has issued tile n - pace_window, so all
-  // workers stream the same few W tiles through L2 (null: no pacing).
+  // Pacing (pair kernel, one chunk: every unit walks the whole vocabulary):
+  // producers publish each vocab tile they have issued in pace[tile] and do
+  // not issue tile n before every unit of the waves so far has issued tile
+  // n - pace_window, so all pairs stream the same few W tiles through L2
+  // (null: no pacing).
   int32_t* pace;
-  int32_t pace_workers;
   int32_t pace_window;
 };
 
@@ -499,7 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t u = q0; u < n_units; u += nq) {
         const Unit w = unit_of(p, u);
         for (int n = w.t0; n < w.t1; ++n) {
-          if (p.pace && rank == 0 && n >= p.pace_window) pace_wait(p.pace + (n - p.pace_window), p.pace_workers);
+          // every unit of the waves so far (full waves of nq pairs, then this one) has issued tile n - window
+          if (p.pace && rank == 0 && n >= p.pace_window)
+            pace_wait(p.pace + (n - p.pace_window), (int32_t)min(n_units, (u / nq + 1) * nq));
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait_bounded(&empty[s], ph ^ 1);
             const uint32_t bar = lm_mapa(smem_u32(&full[s]), 0);
@@ -718,11 +720,15 @@ int launch_lmhead(prorl_ctx* ctx, const void* hidden, int64_t h_stride, const vo
   p.part = ctx->lm_part.as<float>();
   const int64_t units = (int64_t)p.m_tiles * p.n_chunks;
   p.pace = nullptr;
-  if (pair && p.n_chunks == 1 && units <= n_workers && lmhead_pacing() > 0) {
+  // Pacing (one chunk: every unit walks every vocab tile). With more row
+  // tiles than pairs the pairs take them in waves; pace[n] then counts the
+  // issues of tile n over the waves so far, and a unit of wave w waits for the
+  // (w + 1) * pairs (or all) units before it (without this, a second wave ran
+  // at 0.85x of the unfused path: W streamed from HBM by every pair).
+  if (pair && p.n_chunks == 1 && lmhead_pacing() > 0) {
     PRORL_CUDA(ctx->lm_pace.ensure(sizeof(int32_t) * (size_t)p.n_ntiles));
     PRORL_CUDA(cudaMemsetAsync(ctx->lm_pace.p, 0, sizeof(int32_t) * (size_t)p.n_ntiles, st));
     p.pace = ctx->lm_pace.as<int32_t>();
-    p.pace_workers = (int32_t)units;  // one unit per active pair, every pair walks every vocab tile
     p.pace_window = lmhead_pacing();
   }
   if (pair) {
