@@ -154,10 +154,12 @@ def test_score_host_lmhead_mode_matches_materialised_logits(scorer, cuda):
             assert abs(got[i] - ref[i]) <= 1e-5 * max(abs(ref[i]), 1.0), (i, got[i], ref[i])
 
 
-@pytest.mark.parametrize("n,V", [(40000, 8192), (9000, 151936)])
+@pytest.mark.parametrize("n,V", [(40000, 8192), (9000, 151936), (37888, 16384)])
 def test_lmhead_multi_wave_and_paced_schedules(scorer, cuda, n, V):
-    """Row counts that give several waves of CTA-pair units (no pacing) and a
-    single paced wave; sampled rows vs torch fp64."""
+    """Row counts that give several waves of two-chunk CTA-pair units (no
+    pacing), a single paced wave, and two full paced waves of one-chunk units
+    (148 row tiles on 74 pairs: pacing counted across waves); sampled rows vs
+    torch fp64."""
     d = 256
     g = torch.Generator(device=cuda).manual_seed(n)
     H = torch.randn(n, d, device=cuda, generator=g).to(torch.bfloat16)
