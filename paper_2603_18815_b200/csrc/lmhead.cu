@@ -417,6 +417,16 @@ __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate)
       : "memory");
 }
+// one lane of the converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(e));
+  return e != 0;
+}
 // Arrive (once the MMAs issued so far retire) on barrier `bar` in BOTH CTAs of the pair.
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -493,32 +503,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer (both CTAs) =====
+    {  // ===== TMA producer (both CTAs): the warp runs converged, one elected lane issues (as the MMA warp) =====
       const uint64_t pol_h = policy_keep(), pol_w = policy_normal();
       uint32_t s = 0, ph = 0;
       for (int64_t u = q0; u < n_units; u += nq) {
         const Unit w = unit_of(p, u);
         for (int n = w.t0; n < w.t1; ++n) {
           // every unit of the waves so far (full waves of nq pairs, then this one) has issued tile n - window
-          if (p.pace && rank == 0 && n >= p.pace_window)
-            pace_wait(p.pace + (n - p.pace_window), (int32_t)min(n_units, (u / nq + 1) * nq));
+          if (p.pace && rank == 0 && n >= p.pace_window) {
+            if (lane == 0) pace_wait(p.pace + (n - p.pace_window), (int32_t)min(n_units, (u / nq + 1) * nq));
+            __syncwarp();
+          }
           for (int kb = 0; kb < p.n_kb; ++kb) {
             mbar_wait_bounded(&empty[s], ph ^ 1);
             const uint32_t bar = lm_mapa(smem_u32(&full[s]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
-            tma_load_2d_pair(sA + s * A2_BYTES, &tmH, kb * BK, w.m * (2 * BM) + (int)rank * BM, bar, pol_h);
-            tma_load_2d_pair(sB + s * B2_BYTES, &tmW, kb * BK, n * BN + (int)rank * (BN / 2), bar, pol_w);
+            if (elect_one()) {
+              if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2_BYTES);
+              tma_load_2d_pair(sA + s * A2_BYTES, &tmH, kb * BK, w.m * (2 * BM) + (int)rank * BM, bar, pol_h);
+              tma_load_2d_pair(sB + s * B2_BYTES, &tmW, kb * BK, n * BN + (int)rank * (BN / 2), bar, pol_w);
+            }
+            __syncwarp();
             if (++s == STAGES2) {
               s = 0;
               ph ^= 1;
             }
           }
-          if (p.pace && rank == 0) pace_post(p.pace + n);
+          if (p.pace && rank == 0 && lane == 0) pace_post(p.pace + n);
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader only) =====
+    if (rank == 0) {  // ===== MMA issuer (leader only) =====
+      // The whole warp runs the loop converged and one elected lane issues:
+      // the descriptors stay warp-uniform, so ptxas keeps them in uniform
+      // registers. (Issued from a lane-0-only branch, every tcgen05.mma came
+      // with an elect / R2UR.BROADCAST waterfall: ~115 instructions per
+      // 64-deep k-block against 512 cycles of tensor work, which held the
+      // tensor pipe at ~88 % of the active cycles.)
       uint32_t s = 0, ph = 0;
       int tile = 0;
       for (int64_t u = q0; u < n_units; u += nq) {
@@ -533,16 +555,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t ad = umma_desc_sw128(sA + s * A2_BYTES);
             const uint64_t bd = umma_desc_sw128(sB + s * B2_BYTES);
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_pair(d_tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), (kb | k) != 0);
-            umma_commit_pair(&empty[s]);  // both CTAs' stage s free once these MMAs retire
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16_pair(d_tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), (kb | k) != 0);
+              umma_commit_pair(&empty[s]);  // both CTAs' stage s free once these MMAs retire
+            }
+            __syncwarp();
             if (++s == STAGES2) {
               s = 0;
               ph ^= 1;
             }
           }
-          umma_commit_pair(&tfull[acc]);  // both CTAs' accumulators ready
+          if (elect_one()) umma_commit_pair(&tfull[acc]);  // both CTAs' accumulators ready
+          __syncwarp();
         }
       }
     }
