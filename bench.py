@@ -378,27 +378,29 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
     H = torch.randn(n, d, device="cuda", generator=g).to(torch.bfloat16)
     W = (torch.randn(V, d, device="cuda", generator=g) * (2.0 / d ** 0.5)).to(torch.bfloat16)
     t = torch.randint(0, V, (n,), device="cuda", dtype=torch.int32, generator=g)
-    sc.lmhead_logprob(H, W, t)
+    logits = torch.empty((n, V), dtype=torch.bfloat16, device="cuda")
+    # K6 against what it replaces — cuBLAS bf16 GEMM writing the logits to HBM,
+    # then K2 — and against that GEMM alone (the unfused path's floor: a fused
+    # kernel at cuBLAS's GEMM speed with a free epilogue would reach
+    # unfused / gemm); alternating rounds, best of each (the power-capped
+    # clock drifts between rounds)
+    runs = {"k6": lambda: sc.lmhead_logprob(H, W, t),
+            "unfused": lambda: (torch.matmul(H, W.T, out=logits), sc.logprob_entropy(logits, t)),
+            "gemm": lambda: torch.matmul(H, W.T, out=logits)}
+    for f in runs.values():
+        f()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        sc.lmhead_logprob(H, W, t)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    # the unfused baseline it replaces: cuBLAS bf16 GEMM writing the logits to HBM, then K2
-    logits = torch.empty((n, V), dtype=torch.bfloat16, device="cuda")
-    torch.matmul(H, W.T, out=logits)
-    sc.logprob_entropy(logits, t)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        torch.matmul(H, W.T, out=logits)
-        sc.logprob_entropy(logits, t)
-    e1.record()
-    torch.cuda.synchronize()
-    unfused_ms = e0.elapsed_time(e1) / reps
+    best = {k: float("inf") for k in runs}
+    for _ in range(3):
+        for k, f in runs.items():
+            e0.record()
+            for _ in range(reps):
+                f()
+            e1.record()
+            torch.cuda.synchronize()
+            best[k] = min(best[k], e0.elapsed_time(e1) / reps)
+    ms, unfused_ms, gemm_ms = best["k6"], best["unfused"], best["gemm"]
     del logits
     tf = 2.0 * n * d * V / (ms / 1e3) / 1e12
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -409,6 +411,8 @@ def measure_lmhead(sc, c, args, reps: int = 3) -> dict:
             "ms_per_launch": ms, "tflops": tf, "frac_of_measured_bf16_burst": tf / burst,
             "frac_of_measured_bf16_sustained": tf / sustained, "rows_per_s": n / (ms / 1e3),
             "unfused_cublas_gemm_plus_k2_ms": unfused_ms, "speedup_vs_unfused": unfused_ms / ms,
+            "cublas_gemm_alone_ms": gemm_ms, "speedup_vs_gemm_alone": gemm_ms / ms,
+            "fused_ceiling_at_cublas_gemm_speed": unfused_ms / gemm_ms,
             "logits_bytes_avoided": n * V * 2}
 
 

@@ -44,5 +44,8 @@ s.score_host(b.pinned(), cfg, pool, fill=True, seed=3, train=True, grad_pool=gpo
 H = torch.randn(200, 256, device=dev).to(torch.bfloat16)
 W = (torch.randn(4099, 256, device=dev) * 0.1).to(torch.bfloat16)
 s.lmhead_logprob(H, W, torch.randint(0, 4099, (200,), dtype=torch.int32, device=dev))
+# K6 with more 256-row tiles than CTA pairs (75 > 74): the paced multi-wave schedule
+H2 = torch.randn(19200, 256, device=dev).to(torch.bfloat16)
+s.lmhead_logprob(H2, W, torch.randint(0, 4099, (19200,), dtype=torch.int32, device=dev))
 torch.cuda.synchronize()
 print("sanitize workload done")
