@@ -98,11 +98,11 @@ def k_score_stamp() -> str | None:
 
 def k_score_traffic(rows_per_launch: int):
     """(DRAM bytes per launch, note) from profiles/k_score_traffic.json — the
-    `ncu --set full` capture written by scripts/ncu_traffic.py — or (None, why)
+    `ncu --set full` capture summarised by scripts/ncu_summary.py full ... --traffic — or (None, why)
     when that capture was taken on other kernel sources."""
     tf = ROOT / "profiles" / "k_score_traffic.json"
     if not tf.exists():
-        return None, "no capture (scripts/ncu_traffic.py)"
+        return None, "no capture (scripts/ncu_summary.py --traffic)"
     try:
         tj = json.loads(tf.read_text())
     except Exception as ex:

@@ -64,14 +64,32 @@ template <> struct Elem<__nv_bfloat16> {
   }
   // Two logits per step on the packed fp32x2 pipe (FFMA2 / FADD2, sm_100):
   // d = x*c - M, e = 2^d (two MUFU.EX2), S += e, T += d*e.
-  template <int NV>
-  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
+  // kSampled = 1: vector 0 of the group also measures the rounding error of d
+  // (see RoundFix below): d is formed as fl(A + x c_lo) with A = x c_hi - M
+  // exact, which is the same correctly rounded value the single FFMA gives,
+  // and delta = (A - d) + x c_lo is its exact residual; R += e * delta,
+  // Q += e (the sample's own weight).
+  // (kSampled = 2: only the first pair of vector 0 — K2's sample)
+  template <int NV, int kSampled = 0>
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2],
+                                    float2* R = nullptr, float2* Q = nullptr, float2 chi2 = {}, float2 clo2 = {}) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+        if (kSampled && j == 0 && (kSampled > 1 ? q == 0 : true)) {
+          const float2 A = __ffma2_rn(x, chi2, nM2);
+          const float2 d = __ffma2_rn(x, clo2, A);
+          const float2 dl = __ffma2_rn(x, clo2, __fadd2_rn(A, make_float2(-d.x, -d.y)));
+          const float2 e = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+          S[q & 1] = __fadd2_rn(S[q & 1], e);
+          Tt[q & 1] = __ffma2_rn(d, e, Tt[q & 1]);
+          *R = __ffma2_rn(e, dl, *R);
+          *Q = __fadd2_rn(*Q, e);
+          continue;
+        }
         const float2 d = __ffma2_rn(x, c2, nM2);
         const float2 e = make_float2(ex2_approx(d.x), ex2_approx(d.y));
         S[q & 1] = __fadd2_rn(S[q & 1], e);
@@ -111,8 +129,11 @@ template <> struct Elem<float> {
         }
     }
   }
-  template <int NV>
-  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2]) {
+  // fp32 logits: x * c is not exact in fp32, so the split of the bf16 path does
+  // not apply; the sampling arguments are ignored (C1-sized rows only).
+  template <int NV, int kSampled = 0>
+  __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2],
+                                    float2* = nullptr, float2* = nullptr, float2 = {}, float2 = {}) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const float2 xa = make_float2(__uint_as_float(v[j].x), __uint_as_float(v[j].y));
@@ -146,6 +167,47 @@ struct Top {
   float Mx;  // the raw (clamped) logit that set it
 };
 
+// The FFMA that forms d = fl(x c - Mc) rounds once, and for bf16 logits that
+// rounding is not noise: x sits on the bf16 grid and c is fixed, so the bits
+// of x c below ulp(d) repeat the same pattern row after row and the
+// term-weighted mean of the rounding error delta is not zero. Uncorrected it
+// biased every logp by +1.3e-9 (measured over all C2 rows; reproduced by
+// scripts/round_bias_sim.py) — invisible per row, but a 4 100-fold cancelled
+// sum such as sum(old_lp - logp) at C4 saw it as 4.5e-5 relative. Since
+// S_exact = sum 2^(d + delta) = S (1 + ln2 <delta>), <delta> the term-weighted
+// mean rounding error (to 1e-13), a sample of the vectors measures delta
+// exactly (c = c_hi + c_lo with 12-bit c_hi, so x c_hi is exact in fp32 for
+// bf16 x, A = x c_hi - Mc is exact, d = fl(A + x c_lo) is the FFMA's own
+// result and delta = (A - d) + x c_lo) and accumulates R = sum e delta and
+// Q = sum e over the sample; the row end scales S by 1 + ln2 R / Q (a ratio
+// estimate: exact for a row short enough to be sampled whole, ~1e-8 sampling
+// noise per long row that averages out across rows). K2 samples the first
+// pair of the first 16-B vector of every lane group (1/32 of the logits at
+// its default configuration), branch-free: 0.9 % of the C3 bench step at the
+// power-capped clock (a sampled whole vector behind a branch cost 3 %: a
+// second copy of the unrolled group body and 4 more registers). K7 does not
+// sample and does not need to: its 16 warps each sum relative to their own
+// maximum, and its training-mode sums stay within 1e-5 at floor 0 (measured,
+// DESIGN §3); a sampled path in its pass A would have cost it 4-11 %.
+struct RoundFix {
+  float2 chi2, clo2;
+  __device__ __forceinline__ explicit RoundFix(float c) {
+    const float chi = __uint_as_float(__float_as_uint(c) & 0xfffff000u);  // 12 significant bits
+    chi2 = make_float2(chi, chi);
+    clo2 = make_float2(c - chi, c - chi);  // exact
+  }
+  // S scaled by the measured mean rounding error of the warp's sample (whole warp)
+  __device__ __forceinline__ static double apply(double S, float2 R, float2 Q) {
+    float2 rq = make_float2(R.x + R.y, Q.x + Q.y);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rq.x += __shfl_xor_sync(0xffffffffu, rq.x, o);
+      rq.y += __shfl_xor_sync(0xffffffffu, rq.y, o);
+    }
+    return rq.y > 0.f ? S * (1.0 + 0.69314718055994530942 * (double)(rq.x / rq.y)) : S;
+  }
+};
+
 // One lane's share of a row's sums S = sum 2^d, T = sum d 2^d (d = x c - Mc):
 // fp32 accumulators for the current block of chunks (FADD2 / FFMA2 on the
 // packed pipe), folded into fp64 every few chunks, so the fp32 recursive
@@ -153,9 +215,10 @@ struct Top {
 // dominant per-row logp error, ~1e-7 rms at C2).
 struct LaneSums {
   float2 S[2], T[2];
+  float2 R, Q;  // RoundFix sample: sum e * delta, sum e (fp32: only their ratio is used, to ~1e-6)
   double Sd, Td;
   __device__ __forceinline__ void zero() {
-    S[0] = S[1] = T[0] = T[1] = make_float2(0.f, 0.f);
+    S[0] = S[1] = T[0] = T[1] = R = Q = make_float2(0.f, 0.f);
     Sd = Td = 0.0;
   }
   __device__ __forceinline__ void fold() {
@@ -191,10 +254,15 @@ __device__ __forceinline__ int raise_top(float lm, float c, Top& top, LaneSums& 
       a.S[q].x *= sc;
       a.S[q].y *= sc;
     }
+    a.R.x *= sc;
+    a.R.y *= sc;
+    a.Q.x *= sc;
+    a.Q.y *= sc;
     if constexpr (kFolded) {
       const double scd = pow2d(k), dld = (double)dl;
       a.Td = scd * fma(-dld, a.Sd, a.Td);
       a.Sd *= scd;
+
     }
     if (lane == 0) {
       const float d = fmaf(top.Mx, c, -nMc);

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
   rr.init(ring, bars, p.logits, p.stride_bytes, p.rows, p.n_rows, p.vocab, gw, nw, lane);
 
   const float c = p.c;
+  const RoundFix rf(c);
   const uint4 fill = make_uint4(Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord, Elem<T>::kClampWord);
   for (int64_t i = gw; i < p.n_rows; i += nw) {
     const uint8_t* rp = rr.row_ptr(i);
@@ -210,7 +211,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
           const int L = raise_top(lm, c, top, acc, lane);
           if (lane == L) Elem<T>::template mask_first<SUBV>(u, top.Mx);
         }
-        Elem<T>::template accumulate<SUBV>(u, make_float2(c, c), make_float2(-top.Mc, -top.Mc), acc.S, acc.T);
+        const float2 nM2 = make_float2(-top.Mc, -top.Mc);
+        // the RoundFix sample: the first pair of each group's first vector (1/32 of
+        // the bf16 logits at the default configuration), branch-free
+        Elem<T>::template accumulate<SUBV, ES == 2 ? 2 : 0>(u, make_float2(c, c), nM2, acc.S, acc.T, &acc.R, &acc.Q,
+                                                            rf.chi2, rf.clo2);
       }
       // fp64 fold every kFoldVec 16-B vectors per lane (warp-uniform)
       if ((ch + 1) % (kFoldVec / NV) == 0) acc.fold();
@@ -225,6 +230,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
       top = Top{sr.Mc, sr.Mx};
       Sr = sr.Sr;
       Tr = sr.Tr;
+    } else if constexpr (ES == 2) {
+      Sr = RoundFix::apply(Sr, acc.R, acc.Q);  // the FFMA rounding of d (sampled)
     }
     if (lane == 0) {
       const RowStats rs = row_stats(top.Mc, top.Mx, Sr, Tr, xy, c, (double)p.inv_temp);  // fp64 row end

@@ -18,7 +18,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-from tests.parity import REL, SYS_LOGP, partials_report  # noqa: E402
+from tests.parity import REL, partials_report  # noqa: E402
 
 
 def main(path: str) -> None:
@@ -26,9 +26,7 @@ def main(path: str) -> None:
     fx = json.loads((ROOT / "tests" / "golden" / "full_partials.json").read_text())
     out = {"tolerance": {"sums": f"|g - o| <= {REL} |o| (floor 0)", "per_row": f"|g - o| <= {REL} max(|o|, 1e-3)",
                          "counts": "exact; clip counts within the oracle's borderline rows",
-                         "adv_sum": "exactly 0 in real arithmetic: |g - o| <= 1e-9 N_rollouts",
-                         "k1_sum_note": f"the full-size tests add {SYS_LOGP} x n_rows to the k1 bound (documented "
-                                        "systematic residual of the MUFU.EX2 correction, tests/parity.py)"},
+                         "adv_sum": "exactly 0 in real arithmetic: |g - o| <= 1e-9 N_rollouts"},
            "oracle": "oracle/oracle.c oracle_score_batch, fp64 (tests/golden/full_partials.json)",
            "device": "prorl_score_host, fill mode, seed 31, sigma 2.0, 16 576-row micro-batches", "configs": {}}
     for case, d in dev["cases"].items():
