@@ -64,13 +64,11 @@ template <> struct Elem<__nv_bfloat16> {
   }
   // Two logits per step on the packed fp32x2 pipe (FFMA2 / FADD2, sm_100):
   // d = x*c - M, e = 2^d (two MUFU.EX2), S += e, T += d*e.
-  // kSampled = 1: vector 0 of the group also measures the rounding error of d
-  // (see RoundFix below): d is formed as fl(A + x c_lo) with A = x c_hi - M
-  // exact, which is the same correctly rounded value the single FFMA gives,
-  // and delta = (A - d) + x c_lo is its exact residual; R += e * delta,
-  // Q += e (the sample's own weight).
-  // (kSampled = 2: only the first pair of vector 0 — K2's sample)
-  template <int NV, int kSampled = 0>
+  // kSampled: the first pair of vector 0 is the RoundFix sample (see below):
+  // d is formed as fl(A + x c_lo) with A = x c_hi - M exact — the same
+  // correctly rounded value the single FFMA gives — and delta = (A - d) +
+  // x c_lo is its exact residual; R += e * delta, Q += e (the sample's weight).
+  template <int NV, bool kSampled = false>
   __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2],
                                     float2* R = nullptr, float2* Q = nullptr, float2 chi2 = {}, float2 clo2 = {}) {
 #pragma unroll
@@ -79,7 +77,7 @@ template <> struct Elem<__nv_bfloat16> {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float2 x = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
-        if (kSampled && j == 0 && (kSampled > 1 ? q == 0 : true)) {
+        if (kSampled && j == 0 && q == 0) {
           const float2 A = __ffma2_rn(x, chi2, nM2);
           const float2 d = __ffma2_rn(x, clo2, A);
           const float2 dl = __ffma2_rn(x, clo2, __fadd2_rn(A, make_float2(-d.x, -d.y)));
@@ -131,7 +129,7 @@ template <> struct Elem<float> {
   }
   // fp32 logits: x * c is not exact in fp32, so the split of the bf16 path does
   // not apply; the sampling arguments are ignored (C1-sized rows only).
-  template <int NV, int kSampled = 0>
+  template <int NV, bool kSampled = false>
   __device__ static void accumulate(const uint4 (&v)[NV], float2 c2, float2 nM2, float2 (&S)[2], float2 (&Tt)[2],
                                     float2* = nullptr, float2* = nullptr, float2 = {}, float2 = {}) {
 #pragma unroll
@@ -262,7 +260,6 @@ __device__ __forceinline__ int raise_top(float lm, float c, Top& top, LaneSums& 
       const double scd = pow2d(k), dld = (double)dl;
       a.Td = scd * fma(-dld, a.Sd, a.Td);
       a.Sd *= scd;
-
     }
     if (lane == 0) {
       const float d = fmaf(top.Mx, c, -nMc);

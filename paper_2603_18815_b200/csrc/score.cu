@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_score(const ScoreArgs p) {
         const float2 nM2 = make_float2(-top.Mc, -top.Mc);
         // the RoundFix sample: the first pair of each group's first vector (1/32 of
         // the bf16 logits at the default configuration), branch-free
-        Elem<T>::template accumulate<SUBV, ES == 2 ? 2 : 0>(u, make_float2(c, c), nM2, acc.S, acc.T, &acc.R, &acc.Q,
-                                                            rf.chi2, rf.clo2);
+        Elem<T>::template accumulate<SUBV, ES == 2>(u, make_float2(c, c), nM2, acc.S, acc.T, &acc.R, &acc.Q, rf.chi2,
+                                                    rf.clo2);
       }
       // fp64 fold every kFoldVec 16-B vectors per lane (warp-uniform)
       if ((ch + 1) % (kFoldVec / NV) == 0) acc.fold();
