@@ -7,7 +7,9 @@ Cases (SURVEY.md §8 d6 asks for oracle parity on every config):
   * c4r0w8  — configs[3], rank 0 of the 8-GPU group-sharded layout (2 053 469 active rows);
   * c1      — configs[0], the CPU-runnable case (fp32 logits, V = 32 000);
   * c5_wide / c5_narrow — configs[4], the stress sweep at V = 262 144 (64
-    turns) and V = 32 000 (group 32), log-normal 1K-64K-token trajectories.
+    turns) and V = 32 000 (group 32), log-normal 1K-64K-token trajectories;
+  * c5_mid / c5_short — two points inside the sweep: V = 128 256 (group 16,
+    16 turns) and V = 65 536 (group 8, 8 turns, short trajectories).
 
 Each case records the 332 partials, the |term| sums, the count of rows whose
 clip decision sits within 1e-5 of a bound, and a digest of the host SoA so a
@@ -44,6 +46,13 @@ C5_WIDE = dict(index=4, tasks=8, group=4, tokens=16384, turns=64, vocab=262144, 
 C5_NARROW = dict(index=4, tasks=16, group=32, tokens=4096, turns=2, vocab=32000, dtype="bf16", asst_share=0.3,
                  lengths="lognormal", desc="stress: V=32000 bf16, group 32, 1 assistant turn, lognormal 1K-64K tokens")
 
+# and two points inside it: a Llama-3-sized vocabulary with group 16 / 16 turns,
+# and V = 65 536 with group 8 / 8 turns on short (1K-4K) trajectories
+C5_MID = dict(index=4, tasks=8, group=16, tokens=8192, turns=16, vocab=128256, dtype="bf16", asst_share=0.3,
+              lengths="lognormal", desc="stress: V=128256 bf16, group 16, 16 turns, lognormal 1K-64K tokens")
+C5_SHORT = dict(index=4, tasks=32, group=8, tokens=2048, turns=8, vocab=65536, dtype="bf16", asst_share=0.3,
+                lengths="lognormal", desc="stress: V=65536 bf16, group 8, 8 turns, lognormal 1K-64K tokens (mean 2K)")
+
 CASES = {
     "c1": dict(config="c1", kw={}),
     "c2": dict(config="c2", kw={}),
@@ -51,6 +60,8 @@ CASES = {
     "c4r0w8": dict(config="c4", kw={"rank": 0, "world": 8}),
     "c5_wide": dict(config=C5_WIDE, kw={}),
     "c5_narrow": dict(config=C5_NARROW, kw={}),
+    "c5_mid": dict(config=C5_MID, kw={}),
+    "c5_short": dict(config=C5_SHORT, kw={}),
     # non-default options on the C2 batch: sampling temperature 0.7
     # (inv_temperature, types.hpp:59) and the population std (ddof 0)
     "c2_t07_ddof0": dict(config="c2", kw={}, opts={"inv_temperature": 1 / 0.7, "ddof": 0}),

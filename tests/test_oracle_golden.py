@@ -312,3 +312,29 @@ def test_synthetic_plant_is_unbiased():
         d = lp - old
         assert abs(d.mean()) < 0.05, (V, d.mean())
         assert d.min() > -0.27 and d.max() < 0.27, (V, d.min(), d.max())
+
+
+@pytest.mark.parametrize("case", ["c1", "c5_short"])
+def test_full_partials_fixture_is_a_live_oracle_run(case):
+    """The committed full-size oracle partials (tests/golden/full_partials.json,
+    what the GPU full-size parity tests compare against) are what the oracle
+    computes on the same synthetic shard now: the generator's host SoA digest
+    matches and a live oracle_score_batch reproduces the 332 partials (to fp64
+    summation order). The two cheapest cases; the others take minutes."""
+    import os
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    from make_full_partials import CASES, SEED, SIGMA, batch_digest, case_config, case_opts
+
+    from paper_2603_18815_b200 import synth
+    fx = json.loads((Path(__file__).resolve().parent / "golden" / "full_partials.json").read_text())[case]
+    c = CASES[case]
+    sh = synth.make_shard(c["config"], **c["kw"])
+    b = sh.batch
+    assert batch_digest(b) == fx["digest"] and sh.n_active == fx["n_active"]
+    cfg = case_config(case)
+    hb = O.host_batch(b.turns, b.ids, b.lp, b.reward, b.usable, b.group_off, b.rollout_key)
+    r = O.score_batch(hb, O.score_cfg(cfg["vocab"], cfg["dtype"], **case_opts(case)), SEED, SIGMA,
+                      nthreads=os.cpu_count() or 1)
+    assert r["status"] == 0 and r["n_active"] == fx["n_active"] and r["n_border"] == fx["n_border"]
+    np.testing.assert_allclose(r["partials"], np.array(fx["partials"]), rtol=1e-12, atol=1e-9)
